@@ -1,0 +1,143 @@
+/*
+ * shardkrp_cuda.h -- C ABI of the B200-native shardkrp hot path.
+ *
+ * Library: paper_2507_15121_b200/libshardkrp_cuda.so (nvcc, sm_100a only).
+ * Every entry point is extern "C", takes plain pointers, int64 sizes and an
+ * explicit cudaStream_t, and returns an int status (SKRP_OK == 0); the text
+ * of the last failure on the calling thread is read with skrp_last_error.
+ * Device pointers are owned by the caller (torch tensors in the Python host
+ * layer); hot calls never allocate -- scratch is caller-provided, sized by
+ * the matching *_workspace_bytes query.
+ *
+ * Which reference interface each call replaces (paths relative to
+ * /root/reference/pkg/src/shardkrp/):
+ *
+ *   skrp_histogram             partition.py:230  np.bincount(mode_col, minlength=I_d)
+ *   skrp_exclusive_scan_i64    partition.py:164  prefix = [0, cumsum(counts)]
+ *   skrp_equal_index_bounds    partition.py:134-135  _equal_index_bounds
+ *   skrp_nnz_balanced_bounds   partition.py:138-193  _nnz_balanced_bounds (+ _min_max_shard_load)
+ *   skrp_stable_sort_by_key    partition.py:219-220  np.argsort(mode_col, kind="stable")
+ *   skrp_gather_u32            partition.py:221-225  indices[order] / values[order]
+ *   skrp_mttkrp_tiles          kernels.py:109-114 ec_accumulate (+ engine.py:108-125 the
+ *                              per-ISP reduce / atomic disciplines, engine.py:128-212
+ *                              execute_shard) -- the EC hot loop over a device's shards
+ *   skrp_carry_fixup           engine.py:183-187  ordered merge of ISP partial rows
+ *   skrp_mttkrp_host           reference.py:32-68 dense_mttkrp_oracle signature with
+ *                              host buffers (upload, plan, compute, download in one call)
+ *   skrp_synth_*               synth.py:25-93  synth_tensor's laws (uniform / Zipf / values)
+ *   skrp_gram, skrp_apply_rr,
+ *   skrp_col_sumsq, skrp_scale_cols,
+ *   skrp_model_inner           cpd.py:33-105  gram / als_update / fit (+ _model_values_at)
+ */
+#ifndef SHARDKRP_CUDA_H
+#define SHARDKRP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
+
+#define SKRP_OK 0
+#define SKRP_ERR_INVALID 1   /* bad argument       -> ValueError          */
+#define SKRP_ERR_CUDA 2      /* CUDA runtime error -> RuntimeError        */
+#define SKRP_ERR_NOMEM 3     /* workspace too small / allocation failed   */
+#define SKRP_ERR_NONFINITE 4 /* non-finite data    -> FloatingPointError  */
+
+#define SKRP_MAX_MODES 8
+
+#define SKRP_ACC_DETERMINISTIC 0 /* engine.py:12-16 deterministic-reduce */
+#define SKRP_ACC_ATOMIC 1        /* engine.py:17-19 atomic              */
+
+/* ----------------------------------------------------------------- misc */
+int skrp_last_error(char *buf, size_t len);
+int skrp_abi_version(void);
+int skrp_device_sm_count(int *out);
+
+/* ------------------------------------------------------ partition (K2/K3) */
+int skrp_histogram(const uint32_t *keys, int64_t n, int64_t num_bins, int64_t *counts,
+                   skrp_stream_t stream);
+size_t skrp_scan_workspace_bytes(int64_t n);
+int skrp_exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out_n_plus_1, void *workspace,
+                            size_t workspace_bytes, skrp_stream_t stream);
+int skrp_equal_index_bounds(int64_t num_indices, int64_t k, int64_t *bounds_host);
+int skrp_nnz_balanced_bounds(const int64_t *counts_host, int64_t n, int64_t k,
+                             int64_t *bounds_host);
+size_t skrp_sort_workspace_bytes(int64_t n, int key_bits);
+int skrp_stable_sort_by_key(const uint32_t *keys, int64_t n, int key_bits, uint32_t *sorted_keys,
+                            uint32_t *perm, void *workspace, size_t workspace_bytes,
+                            skrp_stream_t stream);
+int skrp_gather_u32(const uint32_t *src, const uint32_t *perm, int64_t n, uint32_t *dst,
+                    skrp_stream_t stream);
+
+/* ------------------------------------------------------------ MTTKRP (K1) */
+typedef struct {
+    int32_t nmodes;                          /* N, 3..SKRP_MAX_MODES                */
+    int32_t mode;                            /* output mode d                       */
+    int32_t rank;                            /* R                                   */
+    int32_t accumulation;                    /* SKRP_ACC_*                          */
+    int64_t nnz;                             /* length of the sorted local arrays   */
+    const uint32_t *coords[SKRP_MAX_MODES];  /* SoA coordinates, sorted by c_d      */
+    const float *values;                     /* fp32 values, same order             */
+    const float *factors[SKRP_MAX_MODES];    /* row-major I_w x R fp32              */
+    float *out;                              /* I_d x R fp32; rows to be written
+                                                must be zero on entry               */
+    const int64_t *tiles;                    /* 2*num_tiles: [start, end) per tile,
+                                                shard order; tiles never straddle an
+                                                ISP (so never a shard)               */
+    int64_t num_tiles;
+    int32_t *carry_rows;                     /* 2*num_tiles (deterministic only)    */
+    float *carry_vals;                       /* 2*num_tiles*R (deterministic only)  */
+    unsigned long long *work_counter;        /* one word of scratch (zeroed here)   */
+    int32_t persistent_ctas;                 /* 0 = #SM x occupancy                 */
+    int32_t variant;                         /* 0 = auto; see mttkrp.cu             */
+} skrp_mttkrp_args;
+
+int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);
+
+/* Segmented reduction of boundary-row carries, one level of the fixed tree.
+ * chunks: 2*n_chunks [begin, end) entry ranges (never straddling a shard);
+ * final_flags[c] != 0: every row of chunk c is complete -> written to out.
+ * Otherwise the chunk's first/last row partials go to rows_out/vals_out at
+ * entries 2c, 2c+1 (-1 rows when absent), in fp64. */
+int skrp_carry_fixup(const int32_t *rows_in, const void *vals_in, int32_t vals_in_is_f64,
+                     const int64_t *chunks, const uint8_t *final_flags, int64_t n_chunks,
+                     int32_t rank, float *out, int32_t *rows_out, double *vals_out,
+                     skrp_stream_t stream);
+
+/* Host-buffer convenience (allocates internally; not a hot call):
+ * indices (nnz x N, uint64, row-major), values float64, factors[w] float64
+ * (I_w x R row-major), out float64 (I_mode x R) -- dense_mttkrp_oracle's
+ * contract computed on the GPU (fp32 arithmetic, fp64 result). */
+int skrp_mttkrp_host(const uint64_t *indices, const double *values, int64_t nnz, int32_t nmodes,
+                     const int64_t *shape, const double *const *factors, int32_t rank,
+                     int32_t mode, double *out, int32_t device);
+
+/* -------------------------------------------------------- synthetic (K7) */
+int skrp_synth_uniform_coords(int32_t *out, int64_t n, int64_t size, uint64_t seed,
+                              int32_t stream_id, skrp_stream_t stream);
+int skrp_synth_zipf_coords(int32_t *out, int64_t n, const double *cdf, int64_t size,
+                           uint64_t seed, int32_t stream_id, skrp_stream_t stream);
+int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed,
+                      skrp_stream_t stream);
+
+/* ---------------------------------------------------------- CP-ALS (K6) */
+int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_stream_t stream);
+int skrp_apply_rr(const float *m, int64_t rows, int32_t rank, const double *w, float *out,
+                  skrp_stream_t stream);
+int skrp_col_sumsq(const float *x, int64_t rows, int32_t rank, double *out,
+                   skrp_stream_t stream);
+int skrp_scale_cols(float *x, int64_t rows, int32_t rank, const double *scale,
+                    skrp_stream_t stream);
+int skrp_model_inner(const uint32_t *const *coords, const float *values, int64_t nnz,
+                     int32_t nmodes, const float *const *factors, const double *lambdas,
+                     int32_t rank, double *out, skrp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHARDKRP_CUDA_H */

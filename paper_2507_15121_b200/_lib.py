@@ -1,0 +1,144 @@
+"""ctypes binding of libshardkrp_cuda.so (include/shardkrp_cuda.h).
+
+The product path has exactly one compute backend: this library.  There is no
+CPU fallback -- if the .so is missing or a call fails, an exception is raised
+(status codes map to the reference's exception types: SKRP_ERR_INVALID ->
+ValueError, SKRP_ERR_NONFINITE -> FloatingPointError, SKRP_ERR_NOMEM ->
+MemoryError, SKRP_ERR_CUDA -> RuntimeError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libshardkrp_cuda.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "shardkrp_cuda.h")
+
+SKRP_OK, SKRP_ERR_INVALID, SKRP_ERR_CUDA, SKRP_ERR_NOMEM, SKRP_ERR_NONFINITE = 0, 1, 2, 3, 4
+SKRP_MAX_MODES = 8
+ACC_DETERMINISTIC, ACC_ATOMIC = 0, 1
+
+vp = ctypes.c_void_p
+i64 = ctypes.c_int64
+i32 = ctypes.c_int32
+u64 = ctypes.c_uint64
+sz = ctypes.c_size_t
+
+
+class MttkrpArgs(ctypes.Structure):
+    _fields_ = [
+        ("nmodes", i32),
+        ("mode", i32),
+        ("rank", i32),
+        ("accumulation", i32),
+        ("nnz", i64),
+        ("coords", vp * SKRP_MAX_MODES),
+        ("values", vp),
+        ("factors", vp * SKRP_MAX_MODES),
+        ("out", vp),
+        ("tiles", vp),
+        ("num_tiles", i64),
+        ("carry_rows", vp),
+        ("carry_vals", vp),
+        ("work_counter", vp),
+        ("persistent_ctas", i32),
+        ("variant", i32),
+    ]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
+    "skrp_abi_version": (i32, []),
+    "skrp_device_sm_count": (i32, [ctypes.POINTER(i32)]),
+    "skrp_histogram": (i32, [vp, i64, i64, vp, vp]),
+    "skrp_scan_workspace_bytes": (sz, [i64]),
+    "skrp_exclusive_scan_i64": (i32, [vp, i64, vp, vp, sz, vp]),
+    "skrp_equal_index_bounds": (i32, [i64, i64, vp]),
+    "skrp_nnz_balanced_bounds": (i32, [vp, i64, i64, vp]),
+    "skrp_sort_workspace_bytes": (sz, [i64, ctypes.c_int]),
+    "skrp_stable_sort_by_key": (i32, [vp, i64, ctypes.c_int, vp, vp, vp, sz, vp]),
+    "skrp_gather_u32": (i32, [vp, vp, i64, vp, vp]),
+    "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
+    "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, vp]),
+    "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),
+    "skrp_synth_uniform_coords": (i32, [vp, i64, i64, u64, i32, vp]),
+    "skrp_synth_zipf_coords": (i32, [vp, i64, vp, i64, u64, i32, vp]),
+    "skrp_synth_values": (i32, [vp, i64, i32, u64, vp]),
+    "skrp_gram": (i32, [vp, i64, i32, vp, vp]),
+    "skrp_apply_rr": (i32, [vp, i64, i32, vp, vp, vp]),
+    "skrp_col_sumsq": (i32, [vp, i64, i32, vp, vp]),
+    "skrp_scale_cols": (i32, [vp, i64, i32, vp, vp]),
+    "skrp_model_inner": (i32, [vp, vp, i64, i32, vp, vp, i32, vp, vp]),
+}
+
+_LIB = None
+
+
+def build(force: bool = False):
+    """Compile the library in-tree for sm_100a (make; nvcc cross-compiles)."""
+    args = ["make", "-s", "-C", _HERE, "-j8"]
+    if force:
+        subprocess.run(["make", "-s", "-C", _HERE, "clean"], check=True)
+    subprocess.run(args, check=True)
+
+
+def lib():
+    """Load the library (fail loudly if absent -- no fallback path exists)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+                "(or __graft_entry__.build()); the shardkrp B200 path has no CPU fallback")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = handle
+    return _LIB
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(512)
+    lib().skrp_last_error(buf, 512)
+    return buf.value.decode(errors="replace")
+
+
+def check(rc: int, name: str):
+    if rc == SKRP_OK:
+        return
+    msg = f"{name}: {last_error()}"
+    if rc == SKRP_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == SKRP_ERR_NONFINITE:
+        raise FloatingPointError(msg)
+    if rc == SKRP_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args):
+    rc = getattr(lib(), name)(*args)
+    check(rc, name)
+    return rc
+
+
+def ptr(t) -> int:
+    """Raw device (or host) address of a torch tensor / numpy array."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream

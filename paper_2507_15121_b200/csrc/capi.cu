@@ -1,0 +1,59 @@
+// capi.cu -- error plumbing and device queries for the C ABI.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace skrp {
+
+static thread_local char g_err[512] = {0};
+static thread_local int g_err_code = 0;
+
+void set_error(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    g_err_code = code;
+}
+
+int cuda_status(cudaError_t e, const char *where)
+{
+    int code = (e == cudaErrorMemoryAllocation) ? SKRP_ERR_NOMEM : SKRP_ERR_CUDA;
+    set_error(code, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+    return code;
+}
+
+int device_sm_count()
+{
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return sms;
+}
+
+}  // namespace skrp
+
+extern "C" {
+
+int skrp_last_error(char *buf, size_t len)
+{
+    if (buf && len) {
+        strncpy(buf, skrp::g_err, len - 1);
+        buf[len - 1] = 0;
+    }
+    return skrp::g_err_code;
+}
+
+int skrp_abi_version(void) { return 1; }
+
+int skrp_device_sm_count(int *out)
+{
+    SKRP_REQUIRE(out != nullptr, "skrp_device_sm_count: null output");
+    int dev = 0;
+    SKRP_CUDA(cudaGetDevice(&dev));
+    SKRP_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev));
+    return SKRP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// common.cuh -- shared helpers for the shardkrp B200 library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/shardkrp_cuda.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "shardkrp_cuda targets sm_100a (B200) only"
+#endif
+
+namespace skrp {
+
+// ------------------------------------------------------------ error plumbing
+void set_error(int code, const char *fmt, ...);
+int cuda_status(cudaError_t e, const char *where);
+
+#define SKRP_REQUIRE(cond, ...)                                   \
+    do {                                                          \
+        if (!(cond)) {                                            \
+            ::skrp::set_error(SKRP_ERR_INVALID, __VA_ARGS__);     \
+            return SKRP_ERR_INVALID;                              \
+        }                                                         \
+    } while (0)
+
+#define SKRP_CUDA(expr)                                           \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::skrp::cuda_status(_e, #expr); \
+    } while (0)
+
+#define SKRP_LAUNCHED(where)                                      \
+    do {                                                          \
+        cudaError_t _e = cudaGetLastError();                      \
+        if (_e != cudaSuccess) return ::skrp::cuda_status(_e, where); \
+    } while (0)
+
+int device_sm_count();
+
+// ------------------------------------------------------------- device utils
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// streaming (read-once) loads: the nonzero stream is touched exactly once per
+// mode, so it must not displace factor rows from L1/L2.
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p, uint64_t pol)
+{
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol)
+{
+    float v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// factor-row gathers: read-only path, L2 evict_last (rows are re-read by
+// other nonzeros; the stream above is evict_first).  VEC floats per lane:
+// 8 = one 256-bit LDG (Blackwell), 4 = LDG.128, 1 = scalar.
+template <int VEC>
+__device__ __forceinline__ void ld_row(float (&v)[VEC], const float *p, uint64_t pol);
+
+template <>
+__device__ __forceinline__ void ld_row<8>(float (&v)[8], const float *p, uint64_t)
+{
+    asm("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                   "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+template <>
+__device__ __forceinline__ void ld_row<4>(float (&v)[4], const float *p, uint64_t pol)
+{
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+}
+
+template <>
+__device__ __forceinline__ void ld_row<1>(float (&v)[1], const float *p, uint64_t pol)
+{
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v[0]) : "l"(p), "l"(pol));
+}
+
+// vector fp32 reduction into global memory (sm_90+): one op per 16 bytes
+__device__ __forceinline__ void red_add_f4(float *p, float4 v)
+{
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so every nonzero's
+// draw is a pure function of (seed, stream, counter) -- no state to carry.
+struct Philox4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                  uint32_t c3, uint32_t k0, uint32_t k1)
+{
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+        uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += W0; k1 += W1;
+    }
+    return {c0, c1, c2, c3};
+}
+
+}  // namespace skrp

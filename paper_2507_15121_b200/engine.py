@@ -1,0 +1,461 @@
+"""Multi-device MTTKRP execution on B200 (drop-in for shardkrp.engine).
+
+Same public surface and semantics as the reference engine (engine.py:45-437):
+``PlatformConfig``, ``DeviceState``, ``make_devices``, ``execute_shard``,
+``mttkrp_mode``, ``mttkrp_all_modes``, ``measure_isolated_compute``,
+``elementwise_compute`` -- plus ``mttkrp(tensor, factors, mode)``, the
+per-mode call with ``dense_mttkrp_oracle``'s contract (reference.py:32-68).
+
+What a "device" is: a logical owner of shards with its own factor replicas
+and output buffer on a physical GPU (device_id mod #GPUs).  Compute is the
+tile kernel (csrc/mttkrp.cu) over the device's shards: a device-side work
+queue of ISP tiles claimed with atomics (the reference's worker pool,
+engine.py:162-209), per-row register accumulation, and the deterministic-
+reduce or atomic discipline for rows shared by two tiles.  Shards are placed
+on devices by the host balancer ``assign_shards``: static round-robin
+(engine.py:291-293) or "dynamic" -- a deterministic replay of the
+reference's claim-next-shard queue (engine.py:267-277) with nnz as the cost,
+i.e. greedy list scheduling in shard order.  After compute, owned rows are
+all-gathered (collective.ring_all_gather in one process; NCCL broadcast of
+owned row ranges across processes, see distributed.py) and, when chained,
+become the mode's factor on every device (engine.py:350-352).
+
+Data stays on the GPU between modes; results come back to the host (float64,
+like the reference) only when asked (``as_numpy=True``, the default).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .collective import FactorPartitionSet, TransferLedger, ring_all_gather
+from .metrics import ModeMetrics, RunMetrics
+from .partition import ModePartitionPlan, PartitionConfig, TensorShard, build_mode_plan, carry_levels, tile_table
+from .tensor import FactorMatrix, NonzeroElement
+
+ACCUMULATION_MODES = ("deterministic-reduce", "atomic")
+SCHEDULING_MODES = ("dynamic", "static")
+
+
+@dataclass(frozen=True)
+class PlatformConfig:
+    devices: int = 1
+    workers_per_device: int = 1
+    column_width: int = 32
+    rank: int = 32
+    accumulation: str = "deterministic-reduce"
+    scheduling: str = "dynamic"
+    # B200 knobs (defaults keep the reference's fields and meaning intact)
+    tile_nnz: int = 1024        # nonzeros per work-queue tile (a slice of one ISP)
+    kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
+    carry_chunk: int = 256      # carry-tree fan-in
+
+    def __post_init__(self):
+        if self.devices < 1 or self.workers_per_device < 1:
+            raise ValueError("devices and workers_per_device must be >= 1")
+        if self.column_width < 1 or self.rank < 1:
+            raise ValueError("column_width and rank must be >= 1")
+        if self.accumulation not in ACCUMULATION_MODES:
+            raise ValueError(f"accumulation must be one of {ACCUMULATION_MODES}")
+        if self.scheduling not in SCHEDULING_MODES:
+            raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
+        if self.tile_nnz < 1 or self.carry_chunk < 2:
+            raise ValueError("tile_nnz must be >= 1 and carry_chunk >= 2")
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DeviceState:
+    """One logical device: factor replicas + output buffer on a GPU."""
+
+    def __init__(self, device_id, factors, output=None, cuda_device=None):
+        torch = _torch()
+        self.device_id = device_id
+        self.cuda_device = cuda_device if cuda_device is not None else (
+            factors[0].device if factors else torch.device("cuda", 0))
+        self.factors = list(factors)
+        self.output = output
+        self.compute_seconds = 0.0
+        self.staging_seconds = 0.0
+        self.shards_processed = 0
+        self.nnz_processed = 0
+        self.owned_ranges = []
+        self.write_rows = None
+
+    def reset_for_mode(self, rows, rank, dtype=None, collect_write_log=False):
+        torch = _torch()
+        self.output = torch.zeros((rows, rank), dtype=dtype or torch.float32, device=self.cuda_device)
+        self.owned_ranges = []
+        self.write_rows = set() if collect_write_log else None
+
+    def __repr__(self):
+        return f"DeviceState(device_id={self.device_id}, gpu={self.cuda_device})"
+
+
+def _as_device_factor(f, dev):
+    torch = _torch()
+    if isinstance(f, FactorMatrix):
+        f = f.data
+    if isinstance(f, torch.Tensor):
+        return f.to(dev, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).to(dev, dtype=torch.float32)
+
+
+def make_devices(factors, cfg: PlatformConfig) -> list:
+    """One DeviceState per device, each with its own fp32 factor replicas
+    (engine.py:83-88); device j lives on GPU j mod torch.cuda.device_count()."""
+    torch = _torch()
+    ngpu = torch.cuda.device_count()
+    if ngpu == 0:
+        raise RuntimeError("make_devices: no CUDA device visible (the B200 engine has no CPU path)")
+    devs = []
+    for j in range(cfg.devices):
+        gpu = torch.device("cuda", j % ngpu)
+        devs.append(DeviceState(j, [_as_device_factor(f, gpu) for f in factors], cuda_device=gpu))
+    return devs
+
+
+def elementwise_compute(x: NonzeroElement, factors, mode: int):
+    """Single-element update (engine.py:91-100): (row, length-R contribution)."""
+    mats = [f.data if isinstance(f, FactorMatrix) else np.asarray(f) for f in factors]
+    contrib = x.value * np.ones(mats[0].shape[1])
+    for w, m in enumerate(mats):
+        if w != mode:
+            contrib = contrib * m[x.indices[w]]
+    return x.indices[mode], contrib
+
+
+# ----------------------------------------------------------------- balancer
+
+
+def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None) -> list:
+    """Shard ids per device.
+
+    static  -- round-robin j::m (engine.py:291-293);
+    dynamic -- the reference's shared claim queue replayed deterministically:
+               shards in order, each to the device that frees up first under
+               cost = nnz (or ``weights``); ties to the lowest device id.
+    """
+    k = plan.shard_count
+    if scheduling == "static":
+        return [list(range(j, k, m)) for j in range(m)]
+    cost = np.array([s.nnz for s in plan.shards] if weights is None else weights, dtype=np.float64)
+    load = np.zeros(m)
+    out = [[] for _ in range(m)]
+    for j in range(k):
+        dev = int(np.argmin(load))
+        out[dev].append(j)
+        load[dev] += cost[j]
+    return out
+
+
+# --------------------------------------------------------- resident tables
+
+
+class _ShardExec:
+    """Device-resident tile table + carry-tree buffers for a set of shards."""
+
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+        torch = _torch()
+        self.gpu = gpu
+        self.rank = rank
+        self.det = cfg.accumulation == "deterministic-reduce"
+        tiles, per_shard = tile_table(plan, shard_ids, cfg.tile_nnz)
+        self.num_tiles = len(tiles) // 2
+        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.tiles = torch.from_numpy(tiles).to(gpu)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
+        self.levels = []
+        if self.det and self.num_tiles:
+            self.carry_rows = torch.empty(2 * self.num_tiles, dtype=torch.int32, device=gpu)
+            self.carry_vals = torch.empty(2 * self.num_tiles * rank, dtype=torch.float32, device=gpu)
+            for table, final in carry_levels(per_shard, cfg.carry_chunk):
+                nch = len(final)
+                lvl = {
+                    "n": nch,
+                    "chunks": torch.from_numpy(table).to(gpu),
+                    "final": torch.from_numpy(final).to(gpu),
+                    "rows_out": None,
+                    "vals_out": None,
+                }
+                if not final.all():
+                    lvl["rows_out"] = torch.empty(2 * nch, dtype=torch.int32, device=gpu)
+                    lvl["vals_out"] = torch.empty(2 * nch * rank, dtype=torch.float64, device=gpu)
+                self.levels.append(lvl)
+        else:
+            self.carry_rows = self.carry_vals = None
+
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
+        """Launch the tile kernel (+ carry tree).  `events` (start, end) CUDA
+        events, if given, bracket the tile kernel alone on `stream`."""
+        if self.num_tiles == 0:
+            return
+        a = _lib.MttkrpArgs()
+        a.nmodes = len(coords)
+        a.mode = mode
+        a.rank = self.rank
+        a.accumulation = _lib.ACC_DETERMINISTIC if self.det else _lib.ACC_ATOMIC
+        a.nnz = nnz_total
+        for w, c in enumerate(coords):
+            a.coords[w] = c.data_ptr()
+            a.factors[w] = None if w == mode else factors[w].data_ptr()
+        a.values = vals.data_ptr()
+        a.out = out.data_ptr()
+        a.tiles = self.tiles.data_ptr()
+        a.num_tiles = self.num_tiles
+        a.carry_rows = self.carry_rows.data_ptr() if self.det else None
+        a.carry_vals = self.carry_vals.data_ptr() if self.det else None
+        a.work_counter = self.counter.data_ptr()
+        a.persistent_ctas = 0
+        a.variant = cfg.kernel_variant
+        if events is not None:
+            events[0].record()  # current stream == `stream` (callers launch on it)
+        _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
+        if events is not None:
+            events[1].record()
+        if not self.det:
+            return
+        rows_in, vals_in, in_f64 = self.carry_rows, self.carry_vals, 0
+        for lvl in self.levels:
+            _lib.call("skrp_carry_fixup", rows_in.data_ptr(), vals_in.data_ptr(), in_f64,
+                      lvl["chunks"].data_ptr(), lvl["final"].data_ptr(), lvl["n"], self.rank,
+                      out.data_ptr(), _lib.ptr(lvl["rows_out"]), _lib.ptr(lvl["vals_out"]), stream)
+            if lvl["rows_out"] is None:
+                break
+            rows_in, vals_in, in_f64 = lvl["rows_out"], lvl["vals_out"], 1
+
+
+def _plan_arrays(plan: ModePartitionPlan, gpu):
+    """The plan's sorted arrays on `gpu` (copied once and cached if the plan
+    was built on another GPU)."""
+    if plan.vals is None:
+        raise ValueError("plan has no device arrays (released)")
+    if plan.vals.device == gpu:
+        return plan.coords, plan.vals
+    key = ("arrays", str(gpu))
+    if key not in plan._exec_cache:
+        plan._exec_cache[key] = ([c.to(gpu) for c in plan.coords], plan.vals.to(gpu))
+    return plan._exec_cache[key]
+
+
+def _shard_exec(plan, shard_ids, cfg, rank, gpu) -> _ShardExec:
+    key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu))
+    ex = plan._exec_cache.get(key)
+    if ex is None:
+        ex = _ShardExec(plan, shard_ids, cfg, rank, gpu)
+        plan._exec_cache[key] = ex
+    return ex
+
+
+def _normalize_ranges(ranges):
+    merged = []
+    for lo, hi in sorted(ranges):
+        if merged and merged[-1][1] == lo:
+            merged[-1] = (merged[-1][0], hi)
+        else:
+            merged.append((lo, hi))
+    return merged
+
+
+def _write_rows(plan, shard_ids, gpu):
+    torch = _torch()
+    coords, _ = _plan_arrays(plan, gpu)
+    rows = set()
+    for j in shard_ids:
+        sh = plan.shards[j]
+        if sh.nnz:
+            rows.update(torch.unique_consecutive(coords[plan.mode][sh.start:sh.stop]).cpu().tolist())
+    return rows
+
+
+def _check_factors(plan, factors):
+    for w, size in enumerate(plan.shape):
+        if factors[w].shape[0] != size:
+            raise ValueError(f"factor for mode {w} has {factors[w].shape[0]} rows, plan needs {size}")
+
+
+def execute_shard(shard: TensorShard, device: DeviceState, mode: int, cfg: PlatformConfig, *,
+                  stream=None, collect_write_log: bool = False, **_ignored):
+    """Run every ISP of one shard on one device (engine.py:128-212).
+
+    The shard's rows are exclusively owned, so its tiles write them directly
+    into ``device.output`` (which must be zero on those rows)."""
+    if shard.mode != mode:
+        raise ValueError(f"shard belongs to mode {shard.mode}, not {mode}")
+    if device.output is None or device.output.shape[1] != device.factors[0].shape[1]:
+        raise ValueError("device output accumulator not initialized for this mode")
+    if shard.nnz == 0:
+        return
+    torch = _torch()
+    plan = shard._plan
+    gpu = device.cuda_device
+    coords, vals = _plan_arrays(plan, gpu)
+    ex = _shard_exec(plan, [shard.shard_id], cfg, device.output.shape[1], gpu)
+    s = stream or torch.cuda.current_stream(gpu)
+    with torch.cuda.device(gpu):
+        ex.run(coords, vals, plan.nnz, mode, device.factors, device.output, cfg, s.cuda_stream)
+    if collect_write_log and device.write_rows is not None:
+        device.write_rows.update(_write_rows(plan, [shard.shard_id], gpu))
+
+
+def mttkrp_mode(plan: ModePartitionPlan, devices: list, cfg: PlatformConfig,
+                ledger: TransferLedger | None = None, *, update_factors: bool = True,
+                collect_write_log: bool = False, as_numpy: bool = True, assignment=None):
+    """One output mode end to end: compute, barrier, all-gather, barrier.
+
+    Returns (gathered output, ModeMetrics) -- float64 numpy like the
+    reference (engine.py:366), or the fp32 device tensor with as_numpy=False.
+    """
+    torch = _torch()
+    m = len(devices)
+    if m != cfg.devices:
+        raise ValueError(f"{m} device states but config says {cfg.devices}")
+    mode = plan.mode
+    rows = plan.shape[mode]
+    rank = devices[0].factors[0].shape[1]
+    _check_factors(plan, devices[0].factors)
+    if m > plan.shard_count:
+        warnings.warn(f"mode {mode}: {m} devices but only {plan.shard_count} shards; surplus devices idle",
+                      RuntimeWarning, stacklevel=2)
+    t_mode = time.perf_counter()
+    ledger = ledger if ledger is not None else TransferLedger()
+    if assignment is None:
+        assignment = assign_shards(plan, m, cfg.scheduling)
+
+    events = []
+    for dev in devices:
+        dev.reset_for_mode(rows, rank, collect_write_log=collect_write_log)
+        dev.compute_seconds = dev.staging_seconds = 0.0
+        dev.shards_processed = dev.nnz_processed = 0
+    for dev, shard_ids in zip(devices, assignment):
+        gpu = dev.cuda_device
+        stream = torch.cuda.current_stream(gpu)
+        coords, vals = _plan_arrays(plan, gpu)
+        ex = _shard_exec(plan, shard_ids, cfg, rank, gpu)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.device(gpu):
+            e0.record(stream)
+            ex.run(coords, vals, plan.nnz, mode, dev.factors, dev.output, cfg, stream.cuda_stream)
+            e1.record(stream)
+        events.append((e0, e1))
+        dev.owned_ranges = [plan.shards[j].index_range for j in shard_ids]
+        dev.shards_processed = len(shard_ids)
+        dev.nnz_processed = ex.nnz
+        if collect_write_log:
+            dev.write_rows = _write_rows(plan, shard_ids, gpu)
+    for (e0, e1), dev in zip(events, devices):
+        e1.synchronize()
+        dev.compute_seconds = e0.elapsed_time(e1) / 1e3  # barrier 1: all shards drained
+
+    ownership = [_normalize_ranges(dev.owned_ranges) for dev in devices]
+    parts = FactorPartitionSet(mode, ownership, [dev.output for dev in devices])
+    gather_before = ledger.total_bytes("allgather")
+    t0 = time.perf_counter()
+    ring_all_gather(parts, ledger)
+    for dev in devices:
+        torch.cuda.current_stream(dev.cuda_device).synchronize()  # barrier 2
+    allgather_seconds = time.perf_counter() - t0
+    if update_factors:
+        for dev in devices:
+            dev.factors[mode] = dev.output
+    metrics = ModeMetrics(
+        mode=mode,
+        device_compute_seconds=[dev.compute_seconds for dev in devices],
+        device_nnz=[dev.nnz_processed for dev in devices],
+        device_shards=[dev.shards_processed for dev in devices],
+        staging_bytes=0,  # plans are resident in HBM: nothing is staged per mode
+        staging_seconds=0.0,
+        allgather_bytes=ledger.total_bytes("allgather") - gather_before,
+        allgather_seconds=allgather_seconds,
+        barrier_count=2,
+        wall_seconds=time.perf_counter() - t_mode,
+    )
+    out = devices[0].output
+    if as_numpy:
+        return out.double().cpu().numpy(), metrics
+    return out, metrics
+
+
+def mttkrp_all_modes(plans: list, devices: list, cfg: PlatformConfig, ledger: TransferLedger | None = None,
+                     *, collect_write_log: bool = False, as_numpy: bool = True):
+    """All modes in ascending order, chained: each mode's gathered output
+    replaces that mode's factor on every device (engine.py:369-400)."""
+    plans = sorted(plans, key=lambda p: p.mode)
+    metrics = RunMetrics(devices=cfg.devices)
+    metrics.preprocessing_seconds = [p.build_time for p in plans]
+    outputs = []
+    t0 = time.perf_counter()
+    for plan in plans:
+        out, mm = mttkrp_mode(plan, devices, cfg, ledger, update_factors=True,
+                              collect_write_log=collect_write_log, as_numpy=as_numpy)
+        outputs.append(out)
+        metrics.modes.append(mm)
+    metrics.wall_seconds = time.perf_counter() - t0
+    return outputs, metrics
+
+
+def measure_isolated_compute(plans: list, factors, cfg: PlatformConfig) -> list:
+    """Per-device compute seconds with each device's static round-robin
+    share run alone on the GPU (engine.py:403-437), timed with CUDA events."""
+    torch = _torch()
+    totals = [0.0] * cfg.devices
+    gpu = torch.device("cuda", torch.cuda.current_device())
+    for plan in sorted(plans, key=lambda p: p.mode):
+        rows = plan.shape[plan.mode]
+        facs = [_as_device_factor(f, gpu) for f in factors]
+        rank = facs[0].shape[1]
+        coords, vals = _plan_arrays(plan, gpu)
+        for j in range(cfg.devices):
+            ids = list(range(j, plan.shard_count, cfg.devices))
+            out = torch.zeros((rows, rank), dtype=torch.float32, device=gpu)
+            ex = _shard_exec(plan, ids, cfg, rank, gpu)
+            s = torch.cuda.current_stream(gpu)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            ex.run(coords, vals, plan.nnz, plan.mode, facs, out, cfg, s.cuda_stream)
+            e1.record(s)
+            e1.synchronize()
+            totals[j] += e0.elapsed_time(e1) / 1e3
+    return totals
+
+
+def _factor_arrays(factors):
+    return [f.data if isinstance(f, FactorMatrix) else f for f in factors]
+
+
+def mttkrp(tensor, factors, mode: int, *, platform: PlatformConfig | None = None,
+           partition: PartitionConfig | None = None, as_numpy: bool = True):
+    """Per-mode MTTKRP with dense_mttkrp_oracle's contract (reference.py:32-68):
+    same validation and messages; float64 (I_mode, R) result computed on the
+    GPU in fp32."""
+    if not 0 <= mode < tensor.num_modes:
+        raise ValueError(f"mode {mode} out of range for {tensor.num_modes}-mode tensor")
+    mats = _factor_arrays(factors)
+    if len(mats) != tensor.num_modes:
+        raise ValueError("need one factor matrix per mode")
+    ranks = {int(m.shape[1]) for m in mats}
+    if len(ranks) != 1:
+        raise ValueError(f"factor ranks differ: {sorted(ranks)}")
+    for w, mtx in enumerate(mats):
+        if mtx.shape[0] != tensor.shape[w]:
+            raise ValueError(f"factor for mode {w} has {mtx.shape[0]} rows, tensor needs {tensor.shape[w]}")
+    rank = ranks.pop()
+    cfg = platform or PlatformConfig(rank=rank)
+    pcfg = partition or PartitionConfig(devices=cfg.devices)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        plan = build_mode_plan(tensor, mode, pcfg, keep_permutation=False)
+        out, _ = mttkrp_mode(plan, make_devices(mats, cfg), cfg, update_factors=False, as_numpy=as_numpy)
+    return out

@@ -1,0 +1,461 @@
+"""Per-mode shard/ISP plans built on the GPU (drop-in for shardkrp.partition).
+
+Same types, fields and semantics as the reference (partition.py:44-262):
+``PartitionConfig``, ``TensorShard``, ``ModePartitionPlan``,
+``build_mode_plan``, ``build_all_plans`` -- including the shard-count clamp
+with its RuntimeWarning (partition.py:209-217), ``index_range`` bounds from
+the equal-index or nnz-balanced strategy, element offsets
+(``searchsorted(sorted_col, bounds, 'left')`` == ``prefix[bounds]``), and ISP
+boundaries ``[0, c, 2c, ..., count]`` (partition.py:127-131).
+
+What moved to the GPU (libshardkrp_cuda.so, csrc/partition.cu):
+  * the stable sort by c_d -- LSD radix on (c_d, position), 8-bit digits;
+    the permutation equals numpy's ``argsort(kind="stable")`` bit-for-bit;
+  * the permuted copy -- SoA u32 coordinates + fp32 values, resident in HBM
+    (the layout the MTTKRP kernel streams);
+  * ``bincount`` + prefix -- histogram and exclusive scan kernels.
+The nnz-balanced cut search runs on the host inside the same library (it is
+O(k log I log nnz) on the prefix array).
+
+Host-visible ``_indices`` (nnz, N) uint64 / ``_values`` are materialised
+lazily on first access (bit-exact: the source tensor's arrays permuted by the
+GPU order), so billion-scale plans never round-trip through host memory.
+"""
+
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .tensor import INDEX_DTYPE, SparseTensorCOO
+
+PLAN_MAGIC = b"SKRPPLN\x00"
+PLAN_VERSION = 1
+STRATEGIES = ("equal-index", "nnz-balanced")
+
+
+class PlanError(Exception):
+    """Base class for plan cache problems (partition.py:32-41)."""
+
+
+class PlanVersionError(PlanError):
+    pass
+
+
+class PlanIntegrityError(PlanError):
+    pass
+
+
+@dataclass(frozen=True)
+class PartitionConfig:
+    devices: int = 1
+    workers_per_device: int = 1
+    oversubscription: int = 4
+    isp_capacity: int = 8192
+    strategy: str = "equal-index"
+
+    def __post_init__(self):
+        for name in ("devices", "workers_per_device", "oversubscription", "isp_capacity"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be a positive integer")
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}, got {self.strategy!r}")
+
+
+def isp_boundaries(count: int, capacity: int) -> np.ndarray:
+    """[0, c, 2c, ..., count]; [0] for an empty shard (partition.py:127-131)."""
+    if count == 0:
+        return np.zeros(1, dtype=np.int64)
+    return np.append(np.arange(0, count, capacity, dtype=np.int64), np.int64(count))
+
+
+class TensorShard:
+    """Contiguous run of plan elements owning one output-index range."""
+
+    def __init__(self, plan, mode, shard_id, index_range, start, stop, isp_bounds):
+        self._plan = plan
+        self.mode = mode
+        self.shard_id = shard_id
+        self.index_range = index_range
+        self.start = start  # element offset of the shard inside the plan
+        self.stop = stop
+        self.isp_boundaries = isp_bounds
+
+    @property
+    def nnz(self) -> int:
+        return self.stop - self.start
+
+    @property
+    def isp_count(self) -> int:
+        return max(len(self.isp_boundaries) - 1, 0)
+
+    def isp_slices(self):
+        b = self.isp_boundaries
+        for q in range(self.isp_count):
+            yield int(b[q]), int(b[q + 1])
+
+    @property
+    def indices(self) -> np.ndarray:
+        return self._plan._indices[self.start:self.stop]
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._plan._values[self.start:self.stop]
+
+    @property
+    def byte_size(self) -> int:
+        return self.nnz * (len(self._plan.shape) * 8 + np.dtype(self._plan.value_dtype).itemsize)
+
+    def __repr__(self):
+        return (f"TensorShard(mode={self.mode}, shard_id={self.shard_id}, "
+                f"index_range={self.index_range}, nnz={self.nnz}, isps={self.isp_count})")
+
+
+class ModePartitionPlan:
+    """Reordered, sharded copy of a tensor for one output mode.
+
+    Device side (HBM): ``coords[w]`` int32 (== u32) sorted by c_mode,
+    ``vals`` fp32, ``perm`` the stable order (int32), ``offsets`` (k+1).
+    """
+
+    def __init__(self, mode, shape, strategy, isp_capacity, name, coords, vals, perm, bounds,
+                 offsets, source=None, build_time=0.0):
+        self.mode = mode
+        self.shape = tuple(shape)
+        self.strategy = strategy
+        self.isp_capacity = isp_capacity
+        self.name = name
+        self.build_time = build_time
+        self.coords = coords
+        self.vals = vals
+        self.perm = perm
+        self.bounds = np.asarray(bounds, dtype=np.int64)
+        self.offsets = np.asarray(offsets, dtype=np.int64)
+        self._source = source
+        self._host_idx = None
+        self._host_vals = None
+        self._exec_cache = {}
+        self.shards = [
+            TensorShard(self, mode, j, (int(self.bounds[j]), int(self.bounds[j + 1])),
+                        int(self.offsets[j]), int(self.offsets[j + 1]),
+                        isp_boundaries(int(self.offsets[j + 1] - self.offsets[j]), isp_capacity))
+            for j in range(len(self.bounds) - 1)
+        ]
+
+    @property
+    def shard_count(self) -> int:
+        return len(self.shards)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.offsets[-1] - self.offsets[0]) if len(self.offsets) else 0
+
+    @property
+    def isp_counts(self) -> list:
+        return [s.isp_count for s in self.shards]
+
+    @property
+    def total_isps(self) -> int:
+        return sum(self.isp_counts)
+
+    @property
+    def value_dtype(self):
+        if self._source is not None and self._source._values is not None:
+            return self._source._values.dtype
+        return np.dtype(np.float32)
+
+    @property
+    def byte_size(self) -> int:
+        return self.nnz * (len(self.shape) * 8 + np.dtype(self.value_dtype).itemsize)
+
+    @property
+    def device_bytes(self) -> int:
+        return self.nnz * 4 * (len(self.shape) + 1)
+
+    # -------------------------------------------------------- host views
+    def order(self) -> np.ndarray:
+        """The stable permutation (== argsort(c_mode, kind="stable"))."""
+        if self.perm is None:
+            raise ValueError("plan was built with keep_permutation=False")
+        return self.perm.cpu().numpy().astype(np.int64)
+
+    @property
+    def _indices(self) -> np.ndarray:
+        if self._host_idx is None:
+            src = self._source
+            if src is not None and src._indices is not None and self.perm is not None:
+                self._host_idx = src._indices[self.order()]
+            else:
+                import torch
+                self._host_idx = torch.stack(self.coords, 1).cpu().numpy().astype(INDEX_DTYPE)
+            self._host_idx.setflags(write=False)
+        return self._host_idx
+
+    @property
+    def _values(self) -> np.ndarray:
+        if self._host_vals is None:
+            src = self._source
+            if src is not None and src._values is not None and self.perm is not None:
+                self._host_vals = src._values[self.order()]
+            else:
+                self._host_vals = self.vals.cpu().numpy()
+            self._host_vals.setflags(write=False)
+        return self._host_vals
+
+    def release_device(self):
+        self.coords = self.vals = self.perm = None
+        self._exec_cache.clear()
+
+    def __repr__(self):
+        return (f"ModePartitionPlan(mode={self.mode}, shape={self.shape}, shards={self.shard_count}, "
+                f"nnz={self.nnz}, strategy={self.strategy!r})")
+
+
+def _key_bits(n: int) -> int:
+    bits = 0
+    while (1 << bits) < n:
+        bits += 1
+    return bits
+
+
+def _shard_bounds(counts_host_fn, num_indices, k, strategy):
+    bounds = np.empty(k + 1, dtype=np.int64)
+    if strategy == "equal-index":
+        _lib.call("skrp_equal_index_bounds", num_indices, k, _lib.ptr(bounds))
+    else:
+        counts = np.ascontiguousarray(counts_host_fn(), dtype=np.int64)
+        _lib.call("skrp_nnz_balanced_bounds", _lib.ptr(counts), num_indices, k, _lib.ptr(bounds))
+    return bounds
+
+
+def build_mode_plan(tensor: SparseTensorCOO, mode: int, cfg: PartitionConfig, *,
+                    keep_permutation: bool = True) -> ModePartitionPlan:
+    """GPU build of the mode-`mode` plan (partition.py:196-257 semantics)."""
+    import torch
+
+    if not 0 <= mode < tensor.num_modes:
+        raise ValueError(f"mode {mode} out of range")
+    t0 = time.perf_counter()
+    num_indices = tensor.shape[mode]
+    k = cfg.devices * cfg.oversubscription
+    if k > num_indices:
+        warnings.warn(f"mode {mode}: requested {k} shards exceeds {num_indices} indices; clamping",
+                      RuntimeWarning, stacklevel=2)
+        k = num_indices
+    coords, vals = tensor.device_arrays()
+    nnz = tensor.nnz
+    if nnz >= 2 ** 32:
+        raise ValueError("per-GPU plan build needs nnz < 2^32 (shard the tensor across GPUs)")
+    dev = vals.device
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    bits = _key_bits(num_indices)
+
+    sorted_coords = [None] * tensor.num_modes
+    key_sorted = torch.empty(nnz, dtype=torch.int32, device=dev)
+    perm = torch.empty(nnz, dtype=torch.int32, device=dev)
+    ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, bits)
+    ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+    _lib.call("skrp_stable_sort_by_key", _lib.ptr(coords[mode]), nnz, bits, _lib.ptr(key_sorted),
+              _lib.ptr(perm), _lib.ptr(ws), ws_bytes, stream)
+    del ws
+    sorted_coords[mode] = key_sorted
+    for w in range(tensor.num_modes):
+        if w != mode:
+            out = torch.empty(nnz, dtype=torch.int32, device=dev)
+            _lib.call("skrp_gather_u32", _lib.ptr(coords[w]), _lib.ptr(perm), nnz, _lib.ptr(out), stream)
+            sorted_coords[w] = out
+    svals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("skrp_gather_u32", _lib.ptr(vals), _lib.ptr(perm), nnz, _lib.ptr(svals), stream)
+
+    # bincount + exclusive prefix on the GPU; offsets = prefix[bounds]
+    counts = torch.empty(num_indices, dtype=torch.int64, device=dev)
+    _lib.call("skrp_histogram", _lib.ptr(coords[mode]), nnz, num_indices, _lib.ptr(counts), stream)
+    prefix = torch.empty(num_indices + 1, dtype=torch.int64, device=dev)
+    sws_bytes = _lib.lib().skrp_scan_workspace_bytes(num_indices)
+    sws = torch.empty(max(int(sws_bytes), 16), dtype=torch.uint8, device=dev)
+    _lib.call("skrp_exclusive_scan_i64", _lib.ptr(counts), num_indices, _lib.ptr(prefix), _lib.ptr(sws),
+              sws_bytes, stream)
+    bounds = _shard_bounds(lambda: counts.cpu().numpy(), num_indices, k, cfg.strategy)
+    offsets = prefix[torch.from_numpy(bounds).to(dev)].cpu().numpy()
+    torch.cuda.current_stream(dev).synchronize()
+    plan = ModePartitionPlan(
+        mode, tensor.shape, cfg.strategy, cfg.isp_capacity, tensor.name, sorted_coords, svals,
+        perm if keep_permutation else None, bounds, offsets, source=tensor,
+        build_time=time.perf_counter() - t0)
+    return plan
+
+
+def build_all_plans(tensor: SparseTensorCOO, cfg: PartitionConfig, *,
+                    keep_permutation: bool = True) -> list:
+    """One independent plan per mode (partition.py:260-262)."""
+    return [build_mode_plan(tensor, d, cfg, keep_permutation=keep_permutation)
+            for d in range(tensor.num_modes)]
+
+
+# ------------------------------------------------------------- work tables
+
+
+def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
+    """[start, end) element ranges of the TILES of the given shards, in order.
+
+    A tile is a slice of one ISP of at most ``tile_nnz`` elements; tiles
+    never straddle an ISP (hence never a shard).  Also returns, per shard,
+    its number of tiles (for the carry-tree chunk tables).
+    """
+    cap = plan.isp_capacity
+    step = max(1, min(tile_nnz, cap))
+    starts, stops, per_shard = [], [], []
+    for j in shard_ids:
+        sh = plan.shards[j]
+        n = sh.nnz
+        if n == 0:
+            per_shard.append(0)
+            continue
+        isp0 = np.arange(0, n, cap, dtype=np.int64)
+        isp1 = np.minimum(isp0 + cap, n)
+        pieces = (isp1 - isp0 + step - 1) // step
+        total = int(pieces.sum())
+        first = np.repeat(np.cumsum(pieces) - pieces, pieces)
+        s = np.repeat(isp0, pieces) + (np.arange(total, dtype=np.int64) - first) * step
+        e = np.minimum(s + step, np.repeat(isp1, pieces))
+        starts.append(s + sh.start)
+        stops.append(e + sh.start)
+        per_shard.append(total)
+    if starts:
+        s = np.concatenate(starts)
+        e = np.concatenate(stops)
+    else:
+        s = e = np.zeros(0, dtype=np.int64)
+    tiles = np.empty(2 * len(s), dtype=np.int64)
+    tiles[0::2] = s
+    tiles[1::2] = e
+    return tiles, np.asarray(per_shard, dtype=np.int64)
+
+
+def carry_levels(tiles_per_shard: np.ndarray, chunk: int = 256):
+    """Chunk tables of the fixed carry-reduction tree.
+
+    Level 1 has 2 entries per tile; a shard's entries are cut into chunks of
+    <= ``chunk`` entries (never crossing shards).  A shard whose entries fit
+    one chunk is FINAL at that level (its rows are complete); otherwise each
+    chunk emits a head and a tail partial to the next level.  The tree is a
+    function of the shard's tile count only, so results do not depend on
+    which device ran the shard.
+    Returns a list of (chunks (2*n int64), final_flags (n uint8)).
+    """
+    levels = []
+    counts = 2 * np.asarray(tiles_per_shard, dtype=np.int64)
+    base = np.concatenate([[0], np.cumsum(counts)[:-1]]) if len(counts) else counts
+    while True:
+        live = counts > 0
+        if not live.any():
+            break
+        nch = np.where(live, (counts + chunk - 1) // chunk, 0)
+        total = int(nch.sum())
+        first = np.repeat(np.cumsum(nch) - nch, nch)
+        local = np.arange(total, dtype=np.int64) - first
+        c0 = np.repeat(base, nch) + local * chunk
+        c1 = np.minimum(c0 + chunk, np.repeat(base + counts, nch))
+        final = np.repeat(nch <= 1, nch).astype(np.uint8)
+        table = np.empty(2 * total, dtype=np.int64)
+        table[0::2] = c0
+        table[1::2] = c1
+        levels.append((table, final))
+        chunk_first = np.cumsum(nch) - nch  # global chunk index of each shard's first chunk
+        counts = np.where(nch > 1, 2 * nch, 0)
+        base = 2 * chunk_first
+    return levels
+
+
+# ------------------------------------------------------------- plan cache
+# Format v1 of partition.py:265-379 (reference), byte-compatible: magic,
+# version, value tag, strategy tag, mode, shape, nnz, capacity, build time,
+# shard table, u64 indices, values, CRC32.
+
+_VALUE_TAG = {np.dtype(np.float64): 8, np.dtype(np.float32): 4}
+_TAG_VALUE = {v: k for k, v in _VALUE_TAG.items()}
+
+
+def save_plan(plan: ModePartitionPlan, path):
+    import struct
+    import zlib
+
+    body = bytearray()
+    body += struct.pack("<I", PLAN_VERSION)
+    body += struct.pack("<B", _VALUE_TAG[np.dtype(plan.value_dtype)])
+    body += struct.pack("<B", STRATEGIES.index(plan.strategy))
+    body += struct.pack("<I", plan.mode)
+    body += struct.pack("<I", len(plan.shape))
+    body += struct.pack(f"<{len(plan.shape)}Q", *plan.shape)
+    body += struct.pack("<QQd", plan.nnz, plan.isp_capacity, plan.build_time)
+    body += struct.pack("<I", plan.shard_count)
+    name = plan.name.encode("utf-8")
+    body += struct.pack("<I", len(name)) + name
+    for s in plan.shards:
+        body += struct.pack("<QQQ", s.index_range[0], s.index_range[1], s.nnz)
+    body += np.ascontiguousarray(plan._indices, dtype=INDEX_DTYPE).tobytes()
+    body += np.ascontiguousarray(plan._values).tobytes()
+    with open(path, "wb") as fh:
+        fh.write(PLAN_MAGIC)
+        fh.write(body)
+        fh.write(struct.pack("<I", zlib.crc32(bytes(body))))
+
+
+def load_plan(path, value_dtype=None, *, device=None) -> ModePartitionPlan:
+    """Read a v1 plan file (checksum + version validated) and upload it."""
+    import struct
+    import zlib
+
+    import torch
+
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < len(PLAN_MAGIC) + 4 or blob[: len(PLAN_MAGIC)] != PLAN_MAGIC:
+        raise PlanVersionError(f"{path}: not a plan cache file")
+    body = blob[len(PLAN_MAGIC):-4]
+    if zlib.crc32(body) != struct.unpack("<I", blob[-4:])[0]:
+        raise PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)")
+    pos = 0
+
+    def take(fmt):
+        nonlocal pos
+        out = struct.unpack_from(fmt, body, pos)
+        pos += struct.calcsize(fmt)
+        return out
+
+    (version,) = take("<I")
+    if version != PLAN_VERSION:
+        raise PlanVersionError(f"{path}: plan version {version}, expected {PLAN_VERSION}")
+    (vtag,) = take("<B")
+    if vtag not in _TAG_VALUE:
+        raise PlanVersionError(f"{path}: unknown value-type tag {vtag}")
+    dtype = _TAG_VALUE[vtag]
+    if value_dtype is not None and np.dtype(value_dtype) != dtype:
+        raise PlanVersionError(f"{path}: plan stores {dtype} values, expected {np.dtype(value_dtype)}")
+    (stag,) = take("<B")
+    (mode,) = take("<I")
+    (nmodes,) = take("<I")
+    shape = take(f"<{nmodes}Q")
+    nnz, capacity, build_time = take("<QQd")
+    (shards,) = take("<I")
+    (nlen,) = take("<I")
+    name = body[pos:pos + nlen].decode("utf-8")
+    pos += nlen
+    table = np.array([take("<QQQ") for _ in range(shards)], dtype=np.int64).reshape(-1, 3)
+    idx = np.frombuffer(body, dtype=INDEX_DTYPE, count=nnz * nmodes, offset=pos).reshape(nnz, nmodes)
+    pos += nnz * nmodes * 8
+    vals = np.frombuffer(body, dtype=dtype, count=nnz, offset=pos)
+    bounds = np.concatenate([table[:, 0], table[-1:, 1]]) if shards else np.zeros(1, dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(table[:, 2])]).astype(np.int64)
+    gpu = device or torch.device("cuda", torch.cuda.current_device())
+    coords = [torch.from_numpy(idx[:, w].astype(np.int32)).to(gpu) for w in range(nmodes)]
+    dvals = torch.from_numpy(vals.astype(np.float32)).to(gpu)
+    plan = ModePartitionPlan(int(mode), tuple(int(s) for s in shape), STRATEGIES[stag], int(capacity), name,
+                             coords, dvals, None, bounds, offsets, build_time=float(build_time))
+    plan._host_idx = idx
+    plan._host_vals = vals
+    return plan

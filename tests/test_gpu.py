@@ -1,0 +1,351 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the pinned oracle.
+
+Bars:
+  * partition / index work: bit-exact (permutation, sorted arrays, bounds,
+    offsets, ISP boundaries);
+  * MTTKRP output: max |gpu - ref| / max(|ref|, 1) <= 1e-4 per mode (fp32,
+    the reference's cli.py:247-261 metric), chained replay for all-mode runs;
+  * deterministic-reduce: bit-identical across device counts and runs.
+"""
+
+import hashlib
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2507_15121_b200 as sk  # noqa: E402
+from paper_2507_15121_b200 import _lib  # noqa: E402
+
+TOL = 1e-4
+NAMES = ["u3", "z3", "z4", "d3", "u5", "s3"]
+
+
+def rel_err(got, expect):
+    if expect.size == 0:
+        return 0.0
+    return float(np.max(np.abs(got - expect) / np.maximum(np.abs(expect), 1.0)))
+
+
+def tensor_from(g, name):
+    s = g("synth.npz")
+    return sk.SparseTensorCOO(tuple(int(x) for x in s[f"{name}_shape"]), s[f"{name}_indices"],
+                              s[f"{name}_values"], name=name)
+
+
+def factors_from(g, name, r, n):
+    s = g("synth.npz")
+    return [sk.FactorMatrix(w, s[f"{name}_F{r}_{w}"]) for w in range(n)]
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ primitives
+
+
+@pytest.mark.parametrize("n,bits", [(1, 1), (100, 3), (4096, 8), (4097, 9), (100_003, 17),
+                                    (1_000_000, 24), (300_000, 0), (65_537, 31)])
+def test_stable_sort_bit_exact(n, bits):
+    rng = np.random.default_rng(n + bits)
+    hi = 1 << bits
+    keys = rng.integers(0, hi, n, dtype=np.int64) if bits else np.zeros(n, dtype=np.int64)
+    if bits > 4:  # heavy duplicates: stability matters
+        keys[rng.random(n) < 0.3] = rng.integers(0, 4)
+    k = torch.from_numpy(keys.astype(np.int32)).cuda()
+    sk_ = torch.empty_like(k)
+    perm = torch.empty_like(k)
+    wsb = _lib.lib().skrp_sort_workspace_bytes(n, bits)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+    _lib.call("skrp_stable_sort_by_key", k.data_ptr(), n, bits, sk_.data_ptr(), perm.data_ptr(),
+              ws.data_ptr(), wsb, stream())
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(perm.cpu().numpy().astype(np.int64), order)
+    assert np.array_equal(sk_.cpu().numpy().astype(np.int64), keys[order])
+
+
+@pytest.mark.parametrize("n,bins", [(10, 1), (1000, 7), (500_000, 16384), (500_000, 16385),
+                                    (2_000_000, 3_000_000)])
+def test_histogram_and_scan(n, bins):
+    rng = np.random.default_rng(bins)
+    keys = (rng.zipf(1.3, n) - 1) % bins
+    k = torch.from_numpy(keys.astype(np.int32)).cuda()
+    counts = torch.empty(bins, dtype=torch.int64, device="cuda")
+    _lib.call("skrp_histogram", k.data_ptr(), n, bins, counts.data_ptr(), stream())
+    expect = np.bincount(keys, minlength=bins)
+    assert np.array_equal(counts.cpu().numpy(), expect)
+    pre = torch.empty(bins + 1, dtype=torch.int64, device="cuda")
+    wsb = _lib.lib().skrp_scan_workspace_bytes(bins)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+    _lib.call("skrp_exclusive_scan_i64", counts.data_ptr(), bins, pre.data_ptr(), ws.data_ptr(), wsb, stream())
+    assert np.array_equal(pre.cpu().numpy(), np.concatenate([[0], np.cumsum(expect)]))
+
+
+# --------------------------------------------------------------------- plans
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_plans_bit_exact(golden, name):
+    t = tensor_from(golden, name)
+    plans = golden("plans.npz")
+    for d in range(t.num_modes):
+        for ci, (m, s, c, st) in enumerate(plans["cfgs"]):
+            cfg = sk.PartitionConfig(devices=int(m), oversubscription=int(s), isp_capacity=int(c),
+                                     strategy="equal-index" if st == 0 else "nnz-balanced")
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                p = sk.build_mode_plan(t, d, cfg)
+            key = f"{name}_m{d}_c{ci}"
+            assert np.array_equal(np.array([s_.index_range for s_ in p.shards]), plans[key + "_ranges"])
+            assert np.array_equal(np.array([s_.nnz for s_ in p.shards]), plans[key + "_nnz"])
+            assert np.array_equal(np.concatenate([s_.isp_boundaries for s_ in p.shards]), plans[key + "_isp"])
+            if ci == 0:
+                assert np.array_equal(p.order(), oracle.stable_order(t.indices, d))
+                assert np.array_equal(p._indices, plans[f"{name}_m{d}_sorted_indices"])
+                assert np.array_equal(p._values, plans[f"{name}_m{d}_sorted_values"])
+                # device copy == the same permutation applied in u32 / fp32
+                dev_idx = torch.stack(p.coords, 1).cpu().numpy().astype(np.uint64)
+                assert np.array_equal(dev_idx, plans[f"{name}_m{d}_sorted_indices"])
+                assert np.array_equal(p.vals.cpu().numpy(),
+                                      plans[f"{name}_m{d}_sorted_values"].astype(np.float32))
+
+
+def test_clamp_warning_matches_reference():
+    t = sk.SparseTensorCOO((2, 3, 3), np.array([[0, 0, 0], [1, 2, 2]]), np.array([1.0, 2.0]))
+    with pytest.warns(RuntimeWarning, match="clamping"):
+        p = sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=2))
+    assert p.shard_count == 2
+
+
+def test_cfg1_plan_digest(golden):
+    meta = golden("cfg1.json")
+    t = sk.synth_tensor((1000, 1000, 1000), 1_000_000, seed=0)
+    assert hashlib.sha256(t.indices.tobytes()).hexdigest() == meta["indices_sha256"]
+    p = sk.build_mode_plan(t, 0, sk.PartitionConfig())
+    assert hashlib.sha256(p.order().tobytes()).hexdigest() == meta["plan_order_sha256"]
+    assert [list(s.index_range) for s in p.shards] == meta["plan_bounds"]
+    assert [s.nnz for s in p.shards] == meta["plan_nnz"]
+    assert p.isp_counts == meta["plan_isps"]
+
+
+# -------------------------------------------------------------------- MTTKRP
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("r", [1, 8, 32])
+def test_mttkrp_matches_oracle(golden, name, r):
+    t = tensor_from(golden, name)
+    fs = factors_from(golden, name, r, t.num_modes)
+    ref = golden("mttkrp.npz")
+    for d in range(t.num_modes):
+        got = sk.mttkrp(t, fs, d)
+        assert got.dtype == np.float64 and got.shape == (t.shape[d], r)
+        assert rel_err(got, ref[f"{name}_R{r}_oracle_{d}"]) <= TOL
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("acc", ["deterministic-reduce", "atomic"])
+@pytest.mark.parametrize("tile", [1, 7, 32, 33, 1024])
+def test_kernel_variants_and_tiles(golden, variant, acc, tile):
+    t = tensor_from(golden, "z3")
+    fs = factors_from(golden, "z3", 32, 3)
+    ref = golden("mttkrp.npz")
+    cfg = sk.PlatformConfig(devices=2, rank=32, accumulation=acc, tile_nnz=tile, kernel_variant=variant)
+    pcfg = sk.PartitionConfig(devices=2, isp_capacity=64)
+    for d in range(3):
+        p = sk.build_mode_plan(t, d, pcfg)
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+        assert rel_err(out, ref[f"z3_R32_oracle_{d}"]) <= TOL
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("m", [1, 3])
+def test_all_modes_chained_replay(golden, name, m):
+    """Chained all-mode run; mode d checked against the oracle replayed on
+    the engine's own previous outputs (cli.py:247-261)."""
+    t = tensor_from(golden, name)
+    fs = factors_from(golden, name, 8, t.num_modes)
+    cfg = sk.PlatformConfig(devices=m, rank=8)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        plans = sk.build_all_plans(t, sk.PartitionConfig(devices=m))
+        outs, metrics = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+    facs = [f.data.copy() for f in fs]
+    for d, out in enumerate(outs):
+        expect = oracle.mttkrp_seq(t.indices, t.values, facs, d)
+        assert rel_err(out, expect) <= TOL
+        facs[d] = out
+    # and the first mode against the reference engine's own chained output
+    assert rel_err(outs[0], golden("mttkrp.npz")[f"{name}_chain_m{m}_0"]) <= TOL
+    assert len(metrics.modes) == t.num_modes
+    assert sum(metrics.modes[0].device_nnz) == t.nnz
+
+
+def test_device_count_invariance_bit_exact(golden):
+    t = tensor_from(golden, "z3")
+    fs = factors_from(golden, "z3", 32, 3)
+    pcfg = sk.PartitionConfig(devices=4, isp_capacity=100)
+    plans = sk.build_all_plans(t, pcfg)
+    results = []
+    for m, sched in [(1, "dynamic"), (2, "static"), (4, "dynamic"), (4, "static"), (1, "dynamic")]:
+        cfg = sk.PlatformConfig(devices=m, rank=32, scheduling=sched, tile_nnz=16)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        results.append(outs)
+    for outs in results[1:]:
+        for a, b in zip(results[0], outs):
+            assert np.array_equal(a, b)
+
+
+def test_write_log_exclusivity(golden):
+    t = tensor_from(golden, "u3")
+    fs = factors_from(golden, "u3", 8, 3)
+    cfg = sk.PlatformConfig(devices=4, rank=8)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4))
+    devs = sk.make_devices(fs, cfg)
+    for p in plans:
+        sk.mttkrp_mode(p, devs, cfg, collect_write_log=True)
+        logs = [d.write_rows for d in devs]
+        for i in range(4):
+            for j in range(i + 1, 4):
+                assert not (logs[i] & logs[j])
+        assert set().union(*logs) == set(np.unique(t.indices[:, p.mode]).tolist())
+
+
+def test_long_rows_many_tiles():
+    """Patents-like: few output rows, each spanning many tiles and ISPs."""
+    t = sk.synth_tensor((3, 300, 300), 200_000, seed=3)
+    fs = sk.random_factors(t.shape, 32, seed=1)
+    for acc in ("deterministic-reduce", "atomic"):
+        cfg = sk.PlatformConfig(rank=32, accumulation=acc, tile_nnz=64, carry_chunk=4)
+        p = sk.build_mode_plan(t, 0, sk.PartitionConfig(isp_capacity=512))
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg)
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, [f.data for f in fs], 0)
+        assert rel_err(out, expect) <= TOL
+
+
+def test_empty_and_single():
+    t0 = sk.SparseTensorCOO((5, 4, 3), np.zeros((0, 3), dtype=np.uint64), np.zeros(0))
+    fs = sk.random_factors(t0.shape, 8, seed=0)
+    assert np.array_equal(sk.mttkrp(t0, fs, 1), np.zeros((4, 8)))
+    t1 = sk.SparseTensorCOO((2, 2, 3), np.array([[0, 1, 2]]), np.array([2.0]))
+    a = np.array([[1.0, 2.0], [0.0, 0.0]])
+    b = np.array([[0.0, 0.0], [3.0, 4.0]])
+    c = np.zeros((3, 2))
+    got = sk.mttkrp(t1, [a, b, c], 2)
+    assert got.tolist() == [[0, 0], [0, 0], [6, 16]]
+
+
+def test_validation_errors_match_reference():
+    t = sk.SparseTensorCOO((2, 2, 3), np.array([[0, 1, 2]]), np.array([2.0]))
+    fs = sk.random_factors(t.shape, 2)
+    with pytest.raises(ValueError, match="out of range"):
+        sk.mttkrp(t, fs, 3)
+    with pytest.raises(ValueError, match="one factor matrix per mode"):
+        sk.mttkrp(t, fs[:2], 0)
+    with pytest.raises(ValueError, match="ranks differ"):
+        sk.mttkrp(t, [fs[0], fs[1], sk.FactorMatrix(2, np.ones((3, 3)))], 0)
+    with pytest.raises(ValueError, match="rows, tensor needs"):
+        sk.mttkrp(t, [fs[0], fs[1], sk.FactorMatrix(2, np.ones((4, 2)))], 0)
+
+
+def test_cfg1_mode0(golden):
+    t = sk.synth_tensor((1000, 1000, 1000), 1_000_000, seed=0)
+    fs = sk.random_factors(t.shape, 32, seed=0)
+    expect = golden("cfg1_mode0.npz")["mode0_oracle"]
+    for acc in ("deterministic-reduce", "atomic"):
+        cfg = sk.PlatformConfig(rank=32, accumulation=acc)
+        p = sk.build_mode_plan(t, 0, sk.PartitionConfig())
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg)
+        assert rel_err(out, expect) <= TOL
+
+
+def test_host_c_abi_entry(golden):
+    """skrp_mttkrp_host: dense_mttkrp_oracle's contract through one C call."""
+    import ctypes
+
+    t = tensor_from(golden, "z4")
+    fs = factors_from(golden, "z4", 8, 4)
+    ref = golden("mttkrp.npz")
+    shape = np.array(t.shape, dtype=np.int64)
+    mats = [np.ascontiguousarray(f.data) for f in fs]
+    fptr = (ctypes.c_void_p * 4)(*[m.ctypes.data for m in mats])
+    for d in range(4):
+        out = np.empty((t.shape[d], 8))
+        _lib.call("skrp_mttkrp_host", t.indices.ctypes.data, np.ascontiguousarray(t.values).ctypes.data,
+                  t.nnz, 4, shape.ctypes.data, fptr, 8, d, out.ctypes.data, torch.cuda.current_device())
+        assert rel_err(out, ref[f"z4_R8_oracle_{d}"]) <= TOL
+
+
+# ---------------------------------------------------------------- collective
+
+
+def test_ring_all_gather_device_buffers(golden):
+    for case in golden("ring.json"):
+        m, rows = case["m"], case["rows"]
+        own = [[tuple(r) for r in o] for o in case["ownership"]]
+        rng = np.random.default_rng(m)
+        truth = rng.random((rows, 2)).astype(np.float32)
+        bufs = []
+        for j in range(m):
+            b = torch.full((rows, 2), -1.0, device="cuda")
+            for lo, hi in own[j]:
+                b[lo:hi] = torch.from_numpy(truth[lo:hi]).cuda()
+            bufs.append(b)
+        parts = sk.FactorPartitionSet(0, own, bufs)
+        ledger = sk.TransferLedger()
+        assert sk.ring_all_gather(parts, ledger) == case["steps"]
+        for b in bufs:
+            assert np.array_equal(b.cpu().numpy(), truth)
+        expect = [(r[0], r[1], r[2], r[3] // 2) for r in case["records"]]  # fp32 vs fp64 bytes
+        assert [(r.step, r.sender, r.receiver, r.byte_count) for r in ledger.records] == expect
+
+
+# --------------------------------------------------------------------- CP-ALS
+
+
+def test_cp_als_rank4_recovery(golden):
+    rng = np.random.default_rng(5)
+    a, b, c = (rng.random((n, 4)) for n in (40, 30, 20))
+    dense = np.einsum("ir,jr,kr->ijk", a, b, c)
+    idx = np.argwhere(np.ones_like(dense, dtype=bool))
+    t = sk.SparseTensorCOO(dense.shape, idx, dense[tuple(idx.T)])
+    model, _ = sk.cp_als(t, 4, 25, seed=0)
+    ref = golden("cpd.npz")["r4_fit"]
+    assert model.fit_history[-1] > 0.99
+    assert abs(model.fit_history[-1] - ref[-1]) < 1e-3
+    assert all(b_ >= a_ - 1e-4 for a_, b_ in zip(model.fit_history, model.fit_history[1:]))
+
+
+def test_cp_als_matches_reference_history(golden):
+    t = sk.synth_tensor((30, 20, 10), 1500, seed=9)
+    ref = golden("cpd.npz")
+    for impl in ("engine", "oracle"):
+        model, _ = sk.cp_als(t, 4, 3, seed=1, mttkrp_impl=impl)
+        assert np.allclose(model.fit_history, ref["u_engine_fit"], rtol=0, atol=2e-4)
+        assert np.allclose(model.lambdas, ref["u_engine_lambdas"], rtol=2e-3)
+
+
+# ------------------------------------------------------------------ generator
+
+
+def test_device_generator_laws():
+    t = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3)
+    idx = t.indices
+    assert idx.max(axis=0).tolist() == [999, 99, 99] and idx.min() == 0
+    assert abs(t.values.mean() - 0.5) < 2e-3 and t.values.min() >= 0 and t.values.max() < 1
+    z = sk.synth_tensor_device((1000, 100, 100), 1_000_000, distribution="zipf", seed=3)
+    cdf = sk.synth.zipf_cdf(1000, 1.2)
+    head = np.mean(z.indices[:, 0] == 0)
+    assert abs(head - cdf[0]) < 3e-3
+    # same seed -> same tensor; other seed -> different
+    t2 = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3)
+    assert np.array_equal(t2.indices, idx)

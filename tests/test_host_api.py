@@ -1,0 +1,234 @@
+"""CPU-side tests: C-ABI library surface, host mirror of the reference API,
+work-table / carry-tree construction, balancer, collectives on host buffers."""
+
+import ctypes
+import hashlib
+import io
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2507_15121_b200 as sk
+from paper_2507_15121_b200 import _lib
+from paper_2507_15121_b200.partition import carry_levels, isp_boundaries, tile_table
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "shardkrp_cuda.h")).read()
+    return sorted(set(re.findall(r"\b(skrp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    if not os.path.exists(_lib.LIB_PATH):
+        _lib.build()
+    handle = ctypes.CDLL(_lib.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for name in syms:
+        assert hasattr(handle, name), name
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes table out of sync with the header"
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (skrp_\w+)", out))
+    assert set(syms) <= exported
+
+
+def test_library_host_entry_points_without_gpu():
+    """Host-only C functions (no device needed): bounds + version + errors."""
+    lib = _lib.lib()
+    assert lib.skrp_abi_version() == 1
+    b = np.empty(3, dtype=np.int64)
+    _lib.call("skrp_equal_index_bounds", 8, 2, b.ctypes.data)
+    assert b.tolist() == [0, 4, 8]
+    with pytest.raises(ValueError):
+        _lib.call("skrp_equal_index_bounds", 8, 0, b.ctypes.data)
+
+
+def test_nnz_balanced_bounds_c_abi_matches_reference(golden):
+    bnd = golden("bounds.npz")
+    for i in range(int(bnd["n_cases"])):
+        counts = np.ascontiguousarray(bnd[f"counts_{i}"], dtype=np.int64)
+        k = int(bnd[f"k_{i}"])
+        out = np.empty(k + 1, dtype=np.int64)
+        _lib.call("skrp_nnz_balanced_bounds", counts.ctypes.data, len(counts), k, out.ctypes.data)
+        assert np.array_equal(out, bnd[f"bounds_{i}"]), i
+
+
+def test_host_synth_matches_reference(golden):
+    s = golden("synth.npz")
+    cases = [("u3", (50, 40, 30), 2000, "uniform", "uniform", 1),
+             ("z3", (1000, 100, 100), 10000, "zipf", "uniform", 0),
+             ("z4", (20, 15, 10, 8), 3000, "zipf", "normal", 3),
+             ("d3", (4, 4, 4), 64, "uniform", "uniform", 2),
+             ("u5", (12, 10, 8, 6, 5), 1500, "uniform", "uniform", 5),
+             ("s3", (7, 300, 9), 1200, "uniform", "normal", 11)]
+    for name, shape, nnz, dist, vd, seed in cases:
+        t = sk.synth_tensor(shape, nnz, distribution=dist, value_dist=vd, seed=seed)
+        assert np.array_equal(t.indices, s[f"{name}_indices"]), name
+        assert np.array_equal(t.values, s[f"{name}_values"]), name
+        for r in (1, 8, 32):
+            for w, f in enumerate(sk.random_factors(shape, r, seed=7)):
+                assert np.array_equal(f.data, s[f"{name}_F{r}_{w}"])
+    t32 = sk.synth_tensor((30, 20, 10), 500, seed=4, value_dtype=np.float32)
+    assert np.array_equal(t32.values, s["f32_values"]) and t32.values.dtype == np.float32
+
+
+def test_cfg1_digests(golden):
+    meta = golden("cfg1.json")
+    t = sk.synth_tensor((1000, 1000, 1000), 1_000_000, "uniform", seed=0)
+    assert hashlib.sha256(t.indices.tobytes()).hexdigest() == meta["indices_sha256"]
+    assert hashlib.sha256(t.values.tobytes()).hexdigest() == meta["values_sha256"]
+    assert t.stats.duplicates == meta["duplicates"]
+    fs = sk.random_factors(t.shape, 32, seed=0)
+    assert [hashlib.sha256(f.data.tobytes()).hexdigest() for f in fs] == meta["factor_sha256"]
+
+
+def test_container_validation_messages():
+    with pytest.raises(ValueError, match="at least 3 modes"):
+        sk.SparseTensorCOO((2, 2), np.zeros((0, 2)), np.zeros(0))
+    with pytest.raises(ValueError, match="positive"):
+        sk.SparseTensorCOO((2, 0, 2), np.zeros((0, 3)), np.zeros(0))
+    with pytest.raises(ValueError, match="negative index"):
+        sk.SparseTensorCOO((2, 2, 2), np.array([[0, -1, 0]]), np.ones(1))
+    with pytest.raises(ValueError, match="out of bounds"):
+        sk.SparseTensorCOO((2, 2, 2), np.array([[0, 2, 0]]), np.ones(1))
+    with pytest.raises(ValueError, match="length mismatch"):
+        sk.SparseTensorCOO((2, 2, 2), np.array([[0, 1, 0]]), np.ones(2))
+    t = sk.SparseTensorCOO((2, 2, 2), np.array([[0, 1, 0]]), np.array([3]))
+    assert t.values.dtype == np.float64 and t.indices.dtype == np.uint64
+    with pytest.raises(ValueError):
+        sk.PartitionConfig(devices=0)
+    with pytest.raises(ValueError):
+        sk.PartitionConfig(strategy="hash")
+    with pytest.raises(ValueError):
+        sk.PlatformConfig(accumulation="lock")
+    with pytest.raises(ValueError):
+        sk.PlatformConfig(scheduling="lottery")
+    with pytest.raises(FloatingPointError):
+        sk.FactorMatrix(0, np.array([[np.inf]])).check_finite()
+
+
+def test_tns_round_trip():
+    text = "# shape: 3 2 4\n2 1 3 1.5\n1 1 1 2.0\n"
+    t = sk.parse_tns(io.StringIO(text))
+    assert t.shape == (3, 2, 4) and t.indices[0].tolist() == [1, 0, 2] and t.values[0] == 1.5
+    buf = io.StringIO()
+    sk.write_tns(t, buf, shape_header=True)
+    t2 = sk.parse_tns(io.StringIO(buf.getvalue()))
+    assert t2 == t
+    c = sk.parse_tns(io.StringIO("1 1 1 2.0\n1 1 1 3.0\n"), coalesce_duplicates=True)
+    assert c.indices.tolist() == [[0, 0, 0]] and c.values.tolist() == [5.0]
+    with pytest.raises(sk.TnsFormatError):
+        sk.parse_tns(io.StringIO("1 1 1 2.0\n1 1 1 3.0\n"))
+    with pytest.raises(sk.TnsFormatError, match="no data lines"):
+        sk.parse_tns(io.StringIO(""))
+
+
+class _FakePlan:
+    def __init__(self, counts, cap):
+        self.isp_capacity = cap
+        off = np.concatenate([[0], np.cumsum(counts)])
+
+        class S:
+            pass
+        self.shards = []
+        for j, c in enumerate(counts):
+            s = S()
+            s.start, s.stop, s.shard_id = int(off[j]), int(off[j + 1]), j
+            s.nnz = int(c)
+            s.isp_boundaries = isp_boundaries(int(c), cap)
+            self.shards.append(s)
+        self.shard_count = len(counts)
+
+
+@pytest.mark.parametrize("counts,cap,tile", [([10, 0, 7, 33], 4, 3), ([1000], 64, 64),
+                                             ([5, 5], 8192, 1024), ([0, 0], 3, 2), ([100, 1], 7, 100)])
+def test_tile_table_respects_isps(counts, cap, tile):
+    plan = _FakePlan(counts, cap)
+    tiles, per = tile_table(plan, list(range(len(counts))), tile)
+    s, e = tiles[0::2], tiles[1::2]
+    assert per.tolist() == [int(np.ceil(c / cap)) * 0 + sum(
+        (min(cap, c - a) + min(tile, cap) - 1) // min(tile, cap) for a in range(0, c, cap)) for c in counts]
+    assert np.all(e > s) and np.all(e - s <= min(tile, cap))
+    # contiguous cover of every shard, and no tile straddles an ISP boundary
+    covered = np.zeros(sum(counts), dtype=int)
+    for a, b in zip(s, e):
+        covered[a:b] += 1
+        j = next(j for j, sh in enumerate(plan.shards) if sh.start <= a < sh.stop)
+        sh = plan.shards[j]
+        assert (a - sh.start) // cap == (b - 1 - sh.start) // cap
+    assert np.all(covered == 1)
+
+
+def test_carry_levels_structure():
+    levels = carry_levels(np.array([3, 0, 1000, 1]), chunk=8)
+    # level 1: shard 0 has 6 entries (1 final chunk), shard 2 2000 entries (250 chunks), shard 3 final
+    t0, f0 = levels[0]
+    assert len(f0) == 1 + 250 + 1
+    assert f0[0] == 1 and f0[-1] == 1 and not f0[1:-1].any()
+    # chunks never cross shard entry ranges
+    ranges = [(0, 6), (6, 6), (6, 2006), (2006, 2008)]
+    for a, b in zip(t0[0::2], t0[1::2]):
+        assert any(lo <= a and b <= hi for lo, hi in ranges)
+    # deeper levels shrink until every shard is final
+    assert levels[-1][1].all()
+    n = [len(f) for _, f in levels]
+    assert n == sorted(n, reverse=True)
+
+
+def test_assign_shards_static_and_dynamic():
+    plan = _FakePlan([10, 1, 1, 1, 10, 1], 4)
+    assert sk.assign_shards(plan, 2, "static") == [[0, 2, 4], [1, 3, 5]]
+    dyn = sk.assign_shards(plan, 2, "dynamic")
+    assert sorted(sum(dyn, [])) == list(range(6))
+    loads = [sum(plan.shards[j].nnz for j in d) for d in dyn]
+    assert max(loads) - min(loads) <= 10
+
+
+def test_ring_all_gather_host_buffers_match_reference_ledger(golden):
+    for case in golden("ring.json"):
+        m, rows = case["m"], case["rows"]
+        own = [[tuple(r) for r in o] for o in case["ownership"]]
+        truth = np.random.default_rng(m).random((rows, 2))
+        bufs = []
+        for j in range(m):
+            b = np.full((rows, 2), -1.0)
+            for lo, hi in own[j]:
+                b[lo:hi] = truth[lo:hi]
+            bufs.append(b)
+        parts = sk.FactorPartitionSet(0, own, bufs)
+        ledger = sk.TransferLedger()
+        assert sk.ring_all_gather(parts, ledger) == case["steps"]
+        assert all(np.array_equal(b, truth) for b in bufs)
+        assert [(r.step, r.sender, r.receiver, r.byte_count, r.kind) for r in ledger.records] == \
+            [tuple(r) for r in case["records"]]
+        assert np.array_equal(sk.gather_broadcast_oracle(parts), truth)
+
+
+def test_partition_set_validation():
+    bufs = [np.zeros((4, 1))] * 2
+    with pytest.raises(ValueError, match="overlap"):
+        sk.FactorPartitionSet(0, [[(0, 3)], [(2, 4)]], bufs).validate()
+    with pytest.raises(ValueError, match="no owner"):
+        sk.FactorPartitionSet(0, [[(0, 1)], [(2, 4)]], bufs).validate()
+
+
+def test_metrics_schema():
+    mm = sk.ModeMetrics(mode=0, device_compute_seconds=[1.0, 3.0], device_nnz=[5, 7], device_shards=[1, 2])
+    rm = sk.RunMetrics(devices=2, modes=[mm], preprocessing_seconds=[0.5])
+    assert rm.compute_seconds == 3.0 and rm.imbalance_pct == 50.0 and rm.nnz_processed == 12
+    recs = sk.run_records(rm, platform=sk.PlatformConfig(devices=2))
+    assert [r["record"] for r in recs] == ["platform", "preprocessing", "device_compute", "device_compute",
+                                           "mode_summary", "imbalance", "totals"]
+
+
+def test_elementwise_compute_spec():
+    a = np.array([[1.0, 2.0], [0.0, 0.0]])
+    b = np.array([[0.0, 0.0], [3.0, 4.0]])
+    row, contrib = sk.elementwise_compute(sk.NonzeroElement((0, 1, 2), 2.0), [a, b, np.zeros((3, 2))], 2)
+    assert row == 2 and contrib.tolist() == [6.0, 16.0]
+    assert sk.khatri_rao([[1.0], [2.0]], [[3.0], [4.0]]).ravel().tolist() == [3.0, 4.0, 6.0, 8.0]

@@ -88,11 +88,11 @@ class DistributedMttkrp:
             return 0
         return 1 + (len(ex.levels) if ex.det else 0)
 
-    def prepare(self, rank_r):
+    def prepare(self, rank_r, dtype=None):
         import torch
 
         self._rank_r = rank_r
-        self.outputs = [torch.empty((p.shape[p.mode], rank_r), dtype=torch.float32, device=self.device)
+        self.outputs = [torch.empty((p.shape[p.mode], rank_r), dtype=dtype or torch.float32, device=self.device)
                         for p in self.plans]
         if self.compute is None:
             for d in range(len(self.plans)):
@@ -104,8 +104,8 @@ class DistributedMttkrp:
         import torch
 
         rank_r = factors[0].shape[1]
-        if self.outputs is None or self._rank_r != rank_r:
-            self.prepare(rank_r)
+        if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
+            self.prepare(rank_r, factors[0].dtype)
         facs = list(factors)
         stream = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
         for d, plan in enumerate(self.plans):

@@ -270,20 +270,23 @@ def run_ours(args, cfg):
     clocks = ClockSampler(gpu_index)
     clocks.start()
     time.sleep(0.3)
-    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in modes]
-           for _ in range(args.steps)]
+    graph = None
+    if world == 1 and not args.no_graph:
+        graph = runner.capture(dev_f)  # whole all-mode step as one CUDA graph
+        graph.replay()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record()
     for k in range(args.steps):
-        runner.run(dev_f, kernel_events=kev[k])
+        if graph is not None:
+            graph.replay()
+        else:
+            runner.run(dev_f)
     e1.record()
     barrier()
     clk = clocks.stop()
     elapsed = e0.elapsed_time(e1) / 1e3
-    kern = [sum(kev[k][i][0].elapsed_time(kev[k][i][1]) for k in range(args.steps)) / 1e3 / args.steps
-            for i in range(len(modes))]
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -292,6 +295,15 @@ def run_ours(args, cfg):
     total_nnz = len(modes) * nnz
     value = total_nnz / step_s
     launches = args.steps * sum(runner.launches_per_mode(i) for i in range(len(modes)))
+
+    # ---- per-kernel device time (eager pass, events on the launching stream)
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in modes]
+           for _ in range(args.steps)]
+    for k in range(args.steps):
+        runner.run(dev_f, kernel_events=kev[k])
+    torch.cuda.synchronize()
+    kern = [sum(kev[k][i][0].elapsed_time(kev[k][i][1]) for k in range(args.steps)) / 1e3 / args.steps
+            for i in range(len(modes))]
 
     # ---- roofline of the tile kernel on this rank
     peak, peak_src = load_peaks()
@@ -310,13 +322,14 @@ def run_ours(args, cfg):
 
     # ---- end to end through the public runner with pinned host buffers
     host_out = [torch.empty((shape[d], R), dtype=torch.float32).pin_memory() for d in modes]
-    runner.run_host(host_f, host_out, dev_f)
+    streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    runner.run_host(host_f, host_out, dev_f, copy_streams=streams)
     barrier()
     x0 = torch.cuda.Event(enable_timing=True)
     x1 = torch.cuda.Event(enable_timing=True)
     x0.record()
     for _ in range(args.steps):
-        h2d, d2h = runner.run_host(host_f, host_out, dev_f)
+        h2d, d2h = runner.run_host(host_f, host_out, dev_f, copy_streams=streams)
     x1.record()
     barrier()
     e2e_s = x0.elapsed_time(x1) / 1e3 / args.steps
@@ -350,8 +363,9 @@ def run_ours(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "shape": list(shape), "nnz": nnz, "rank": R,
                        "modes": modes, "partition": f"{cfg['strategy']}, devices={world}, oversub 4, ISP 8192",
-                       "accumulation": args.accumulation, "tile_nnz": args.tile,
+                       "accumulation": args.accumulation, "tile_nnz": runner._exec(0, R).tile_nnz,
                        "parallelism": f"output-row shards x{world}",
+                       "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -434,11 +448,12 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accumulation", default="deterministic-reduce", choices=("deterministic-reduce", "atomic"))
-    ap.add_argument("--tile", type=int, default=1024)
+    ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--parity-rows", type=int, default=512)
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         print("note: warmup < 3 is below the timing rules; proceeding", file=sys.stderr)

@@ -52,6 +52,10 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 #define SKRP_ACC_DETERMINISTIC 0 /* engine.py:12-16 deterministic-reduce */
 #define SKRP_ACC_ATOMIC 1        /* engine.py:17-19 atomic              */
 
+/* skrp_mttkrp_args.flags */
+#define SKRP_FLAG_ADDITIVE 1     /* rows may also get contributions from other tile
+                                    groups (blocked layouts): every flush adds   */
+
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
 int skrp_abi_version(void);
@@ -94,6 +98,7 @@ typedef struct {
     unsigned long long *work_counter;        /* one word of scratch (zeroed here)   */
     int32_t persistent_ctas;                 /* 0 = #SM x occupancy                 */
     int32_t variant;                         /* 0 = auto; see mttkrp.cu             */
+    int32_t flags;                           /* SKRP_FLAG_* bits                    */
 } skrp_mttkrp_args;
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);

@@ -20,6 +20,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "shardkrp_cuda.h")
 SKRP_OK, SKRP_ERR_INVALID, SKRP_ERR_CUDA, SKRP_ERR_NOMEM, SKRP_ERR_NONFINITE = 0, 1, 2, 3, 4
 SKRP_MAX_MODES = 8
 ACC_DETERMINISTIC, ACC_ATOMIC = 0, 1
+FLAG_ADDITIVE = 1
 
 vp = ctypes.c_void_p
 i64 = ctypes.c_int64
@@ -46,6 +47,7 @@ class MttkrpArgs(ctypes.Structure):
         ("work_counter", vp),
         ("persistent_ctas", i32),
         ("variant", i32),
+        ("flags", i32),
     ]
 
 

@@ -62,8 +62,8 @@ __device__ __forceinline__ void red_vec(float *p, const float (&v)[VEC])
 // NM: number of modes (0 = runtime, <= SKRP_MAX_MODES)
 // VEC: floats per lane per row chunk; LPN: lanes per nonzero (power of two);
 // CH: row chunks per lane (R <= VEC * LPN * CH); U: steps per group.
-template <int NM, int VEC, int LPN, int CH, int U>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) mttkrp_tiles_kernel(const skrp_mttkrp_args a)
+template <int NM, int VEC, int LPN, int CH, int U, int MINB = 1>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) mttkrp_tiles_kernel(const skrp_mttkrp_args a)
 {
     constexpr int S = 32 / LPN;   // nonzero slots per warp
     constexpr int G = S * U;      // nonzeros per group
@@ -240,6 +240,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mttkrp_tiles_kernel(const s
     }
 }
 
+#include "mttkrp_v2.cuh"
+
 // ------------------------------------------------------------ carry fixup
 // One warp per chunk; lanes own columns; fp64 running sums; rows ascend.
 template <typename VT>
@@ -307,26 +309,52 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const int32_t *__restr
 
 // --------------------------------------------------------------- dispatch
 using KernelFn = void (*)(const skrp_mttkrp_args);
+using KernelV2 = void (*)(const skrp_mttkrp_args, int);
 
 struct Variant {
-    KernelFn fn;
-    int vec, lpn, ch;
+    KernelFn fn = nullptr;   // legacy tile kernel (generic shapes, A/B variants)
+    KernelV2 v2 = nullptr;   // production kernel
+    size_t smem = 0;
 };
 
-template <int NM, int VEC, int LPN, int CH, int U>
+template <int NM, int VEC, int LPN, int CH, int U, int MINB = 1>
 static Variant mk()
 {
-    return {mttkrp_tiles_kernel<NM, VEC, LPN, CH, U>, VEC, LPN, CH};
+    Variant v;
+    v.fn = mttkrp_tiles_kernel<NM, VEC, LPN, CH, U, MINB>;
+    return v;
 }
 
-// Fast variants: R % 8 == 0, 256-bit row loads, one row chunk per lane.
+template <int NM, int LPN, int U, int MINB>
+static Variant mk2()
+{
+    Variant v;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB>;
+    v.smem = v2_smem_bytes<8 * LPN>();
+    return v;
+}
+
+template <int NM>
+static bool pick_v2(int R, Variant &v)
+{
+    switch (R) {
+    case 8: v = mk2<NM, 1, 1, 3>(); return true;
+    case 16: v = mk2<NM, 2, (NM == 3 ? 2 : 1), 3>(); return true;
+    case 32: v = mk2<NM, 4, 2, 3>(); return true;
+    case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2>(); return true;
+    case 128: v = mk2<NM, 16, (NM == 3 ? 2 : 1), 2>(); return true;
+    default: return false;
+    }
+}
+
+// Legacy fast variants: R % 8 == 0, 256-bit row loads, one row chunk per lane.
 template <int NM>
 static bool pick_fast(int R, Variant &v)
 {
     switch (R) {
     case 8: v = mk<NM, 8, 1, 1, 1>(); return true;
     case 16: v = mk<NM, 8, 2, 1, 2>(); return true;
-    case 32: v = mk<NM, 8, 4, 1, 4>(); return true;
+    case 32: v = mk<NM, 8, 4, 1, 4, 3>(); return true;
     case 64: v = mk<NM, 8, 8, 1, 4>(); return true;
     case 128: v = mk<NM, 8, 16, 1, 2>(); return true;
     case 256: v = mk<NM, 8, 32, 1, 1>(); return true;
@@ -361,6 +389,8 @@ static Variant pick_generic(int R)
 
 static bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
+// variant: 0 auto (production kernel where it applies), 1 generic scalar,
+// 2 legacy LDG.128, 6 legacy LDG.256
 static Variant choose(const skrp_mttkrp_args &a)
 {
     Variant v{};
@@ -368,6 +398,19 @@ static Variant choose(const skrp_mttkrp_args &a)
     for (int w = 0; w < a.nmodes; ++w) al32 = al32 && (w == a.mode || aligned(a.factors[w], 32));
     if (a.accumulation == SKRP_ACC_DETERMINISTIC) al32 = al32 && aligned(a.carry_vals, 32);
     if (al32 && a.variant != 1) {
+        if (a.variant == 7 && a.rank == 32) {  // occupancy A/B for the production kernel
+            if (a.nmodes == 3) return mk2<3, 4, 2, 2>();
+            if (a.nmodes == 4) return mk2<4, 4, 2, 2>();
+        }
+        if (a.variant == 8 && a.rank == 32) {
+            if (a.nmodes == 3) return mk2<3, 4, 4, 2>();
+            if (a.nmodes == 4) return mk2<4, 4, 4, 2>();
+        }
+        if (a.variant == 0) {
+            if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;
+            if (a.nmodes == 4 && pick_v2<4>(a.rank, v)) return v;
+            if (a.nmodes == 5 && pick_v2<5>(a.rank, v)) return v;
+        }
         if (a.variant == 2) {
             if (a.nmodes == 3 && pick_vec4<3>(a.rank, v)) return v;
             if (a.nmodes == 4 && pick_vec4<4>(a.rank, v)) return v;
@@ -403,13 +446,26 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
         SKRP_REQUIRE(a.carry_rows && a.carry_vals, "deterministic accumulation needs carry buffers");
 
     cudaStream_t s = (cudaStream_t)stream;
+    SKRP_REQUIRE(!(a.flags & SKRP_FLAG_ADDITIVE) || a.accumulation == SKRP_ACC_ATOMIC,
+                 "additive (blocked-layout) execution needs atomic accumulation");
     Variant v = choose(a);
+    SKRP_REQUIRE(!(a.flags & SKRP_FLAG_ADDITIVE) || v.v2, "additive execution needs R in {8,16,32,64,128} and N <= 5");
     int occ = 0;
-    SKRP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, kWarpsPerCta * 32, 0));
+    if (v.v2) {
+        if (v.smem > 48 * 1024)
+            SKRP_CUDA(cudaFuncSetAttribute(v.v2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+        SKRP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.v2, kWarpsPerCta * 32, v.smem));
+    } else {
+        SKRP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, kWarpsPerCta * 32, 0));
+    }
     int64_t ctas = a.persistent_ctas > 0 ? a.persistent_ctas : (int64_t)device_sm_count() * std::max(occ, 1);
     ctas = std::min<int64_t>(ctas, (a.num_tiles + kWarpsPerCta - 1) / kWarpsPerCta);
     SKRP_CUDA(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), s));
-    v.fn<<<(unsigned)std::max<int64_t>(ctas, 1), kWarpsPerCta * 32, 0, s>>>(a);
+    unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
+    if (v.v2)
+        v.v2<<<grid, kWarpsPerCta * 32, v.smem, s>>>(a, (a.flags & SKRP_FLAG_ADDITIVE) ? 1 : 0);
+    else
+        v.fn<<<grid, kWarpsPerCta * 32, 0, s>>>(a);
     SKRP_LAUNCHED("mttkrp_tiles_kernel");
     return SKRP_OK;
 }

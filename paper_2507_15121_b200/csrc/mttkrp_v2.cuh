@@ -1,0 +1,243 @@
+// mttkrp_v2.cuh -- the production tile kernel (R % 8 == 0, 8 <= R <= 256).
+//
+// Same contract and flush rules as mttkrp_tiles_kernel (mttkrp.cu), tuned for
+// instruction economy and for short row runs:
+//   * slot s (LPN lanes, one 256-bit LDG per lane per row) handles the U
+//     CONSECUTIVE nonzeros s*U .. s*U+U-1 of a 32-nonzero batch; full batches
+//     run without per-element predicates;
+//   * the Hadamard product is folded into the accumulation with FFMA
+//     (acc = fma(v*F_w1*..., F_wlast, acc)) -- one FMUL + one FFMA per float
+//     at N = 3;
+//   * batches whose 32 rows all equal the running row accumulate in registers
+//     (long runs: FLYCOO order, 354..944 nonzeros per row at cfg2);
+//   * other batches number their distinct rows with one ballot + popc, add
+//     every contribution into a per-warp shared-memory row buffer with
+//     red.shared (rows padded to R+1 floats: conflict-free across rows), then
+//     write each completed row once with the whole warp (one coalesced 128-B
+//     store/red per 32 columns) and carry the last row into the registers;
+//   * ADDITIVE mode (blocked execution layouts, where other tile groups also
+//     contribute to a row) turns every flush into red.global.add.
+#pragma once
+
+#include <type_traits>
+
+template <int NM, int LPN, int U, int MINB>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
+    mttkrp_v2_kernel(const skrp_mttkrp_args a, int additive)
+{
+    constexpr int VEC = 8;
+    constexpr int S = 32 / LPN;     // nonzero slots per warp
+    constexpr int G = S * U;        // nonzeros per group
+    constexpr int RR = VEC * LPN;   // rank handled by this instantiation
+    constexpr int STR = RR + 4;     // staging row stride (floats), keeps 16-B alignment
+    constexpr int NIN = NM - 1;     // input modes per nonzero
+    constexpr int CPL = (RR + 31) / 32;  // columns per lane in the column layout
+    static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
+    extern __shared__ __align__(16) float smem_v2[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    float *stage = smem_v2 + (size_t)wib * (33 * STR);  // 32 nonzero rows + 1 carry row
+    float *carry_row = stage + 32 * STR;
+    const int slot = lane / LPN, sl = lane % LPN;
+    const int col = sl * VEC;
+    const int mode = a.mode;
+    const uint32_t *__restrict__ rowc = a.coords[mode];
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_row = policy_evict_last();
+    const bool det = a.accumulation == SKRP_ACC_DETERMINISTIC;
+    // input modes in ascending order (kernels.py:63-69): j-th input = j or j+1
+    const float *__restrict__ F[NIN];
+    const uint32_t *__restrict__ C[NIN];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) {
+        const int w = j < mode ? j : j + 1;
+        F[j] = a.factors[w];
+        C[j] = a.coords[w];
+    }
+
+    for (;;) {
+        unsigned long long claimed = 0;
+        if (lane == 0) claimed = atomicAdd(a.work_counter, 1ull);
+        const int64_t t = (int64_t)__shfl_sync(kFull, claimed, 0);
+        if (t >= a.num_tiles) break;
+        const int64_t b0 = a.tiles[2 * t], b1 = a.tiles[2 * t + 1];
+        const int64_t prev_row = b0 > 0 ? (int64_t)rowc[b0 - 1] : -1;
+        const int64_t next_row = b1 < a.nnz ? (int64_t)rowc[b1] : -1;
+        if (det && lane == 0) {
+            a.carry_rows[2 * t] = -1;
+            a.carry_rows[2 * t + 1] = -1;
+        }
+        uint32_t cur = rowc[b0];
+        bool head = true;
+        float acc[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+
+        auto reduce_slots = [&]() {
+#pragma unroll
+            for (int off = LPN; off < 32; off <<= 1)
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
+        };
+        // register-layout row write (after reduce_slots slot 0 holds the row)
+        auto write_regs = [&](uint32_t row, bool is_head, bool is_tail) {
+            const bool shared = (is_head && prev_row == (int64_t)row) || (is_tail && next_row == (int64_t)row);
+            if (slot == 0) {
+                float *dst = a.out + (size_t)row * RR + col;
+                if (shared && det) {
+                    const int64_t entry = 2 * t + (is_head ? 0 : 1);
+                    store_vec<VEC>(a.carry_vals + (size_t)entry * RR + col, acc);
+                    if (lane == 0) a.carry_rows[entry] = (int32_t)row;
+                } else if (shared || additive) {
+                    red_vec<VEC>(dst, acc);
+                } else {
+                    store_vec<VEC>(dst, acc);
+                }
+            }
+        };
+        // column-layout row write (lane owns columns lane, lane+32, ...)
+        auto write_cols = [&](uint32_t row, const float (&v)[CPL], bool is_head) {
+            const bool shared = is_head && prev_row == (int64_t)row;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = lane + 32 * q;
+                if (c < RR) {
+                    if (shared && det) a.carry_vals[(size_t)(2 * t) * RR + c] = v[q];
+                    else if (shared || additive) atomicAdd(a.out + (size_t)row * RR + c, v[q]);
+                    else a.out[(size_t)row * RR + c] = v[q];
+                }
+            }
+            if (shared && det && lane == 0) a.carry_rows[2 * t] = (int32_t)row;
+        };
+
+        for (int64_t base = b0; base < b1; base += 32) {
+            const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
+            const bool lv = lane < nin;
+            const uint32_t r_l = lv ? ld_stream_u32(rowc + base + lane, pol_stream) : 0xffffffffu;
+            const float v_l = lv ? ld_stream_f32(a.values + base + lane, pol_stream) : 0.f;
+            uint32_t c_l[NIN];
+#pragma unroll
+            for (int j = 0; j < NIN; ++j) c_l[j] = lv ? ld_stream_u32(C[j] + base + lane, pol_stream) : 0u;
+            const bool uniform = __all_sync(kFull, !lv || r_l == cur);
+
+            // one group of G nonzeros: slot s takes g0 + s*U .. + U-1.
+            // FULL groups carry no per-element predicates.
+            auto group = [&](int g0, auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                float g[U][NIN][VEC];
+                float vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = g0 + slot * U + u;
+                    vv[u] = __shfl_sync(kFull, v_l, e);
+#pragma unroll
+                    for (int j = 0; j < NIN; ++j) {
+                        const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
+                        if (FULL || e < nin) ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
+                    }
+                }
+                if (uniform) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (FULL || g0 + slot * U + u < nin) {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                float p = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN - 1; ++j) p *= g[u][j][i];
+                                acc[i] = fmaf(p, g[u][NIN - 1][i], acc[i]);
+                            }
+                        }
+                    }
+                } else {
+                    // stage each nonzero's contribution row (plain stores)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = g0 + slot * U + u;
+                        if (FULL || e < nin) {
+                            float p[VEC];
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                p[i] = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN; ++j) p[i] *= g[u][j][i];
+                            }
+                            store_vec<VEC>(stage + e * STR + col, p);
+                        }
+                    }
+                }
+            };
+
+            bool row0_is_cur = true;
+            unsigned cm = 0;
+            if (!uniform) {
+                const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
+                const uint32_t up = __shfl_up_sync(kFull, r_l, 1);
+                cm = __ballot_sync(kFull, lv && lane > 0 && r_l != up);  // row starts after nonzero 0
+                row0_is_cur = row0 == cur;
+                reduce_slots();
+                if (!row0_is_cur) {
+                    write_regs(cur, head, false);
+                    head = false;
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+                }
+                if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+            }
+            if (nin == 32) {
+#pragma unroll 1
+                for (int g0 = 0; g0 < 32; g0 += G) group(g0, std::integral_constant<bool, true>{});
+            } else {
+#pragma unroll 1
+                for (int g0 = 0; g0 < nin; g0 += G) group(g0, std::integral_constant<bool, false>{});
+            }
+            if (uniform) continue;
+
+            // segmented sums over the staged rows, lanes own columns
+            __syncwarp();
+            float run[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = lane + 32 * q;
+                run[q] = (c < RR) ? carry_row[c] : 0.f;
+            }
+            // the open row: cur continued by nonzero 0, or the row nonzero 0 opens
+            uint32_t row = row0_is_cur ? cur : __shfl_sync(kFull, r_l, 0);
+            bool rhead = row0_is_cur && head;  // tile head only while the first row is open
+            for (int e = 0; e < nin; ++e) {
+                if ((cm >> e) & 1u) {
+                    write_cols(row, run, rhead);
+                    rhead = false;
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) run[q] = 0.f;
+                    row = __shfl_sync(kFull, r_l, e);
+                }
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < RR) run[q] += stage[e * STR + c];
+                }
+            }
+            // the last row stays open: back to the register layout (slot 0)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = lane + 32 * q;
+                if (c < RR) carry_row[c] = run[q];
+            }
+            __syncwarp();
+            cur = row;
+            head = rhead;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
+            __syncwarp();
+        }
+        reduce_slots();
+        write_regs(cur, head, true);
+    }
+}
+
+template <int RR>
+constexpr size_t v2_smem_bytes()
+{
+    return sizeof(float) * kWarpsPerCta * (33 * (RR + 4));
+}

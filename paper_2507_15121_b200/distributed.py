@@ -98,9 +98,12 @@ class DistributedMttkrp:
             for d in range(len(self.plans)):
                 self._exec(d, rank_r)
 
-    def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None):
+    def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None,
+            after_mode=None):
         """All modes; `factors` are this rank's full fp32 factor replicas.
-        Returns the list of gathered outputs (device tensors, reused)."""
+        Returns the list of gathered outputs (device tensors, reused).
+        ``after_mode(i, out)`` is called once mode i's output is gathered
+        (stream-ordered), e.g. to start its device-to-host copy."""
         import torch
 
         rank_r = factors[0].shape[1]
@@ -121,21 +124,69 @@ class DistributedMttkrp:
                                           stream.cuda_stream, events=ev)
             if self.world > 1:
                 allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
+            if after_mode is not None:
+                after_mode(d, out)
             if chained:
                 facs[plan.mode] = out
         return self.outputs
 
-    def run_host(self, host_factors, host_outputs, dev_factors, chained=True):
-        """End-to-end step with HOST buffers: H2D factors (pinned), all modes,
-        D2H every gathered output (pinned).  Returns bytes (h2d, d2h)."""
+    def needed_factors(self, chained=True):
+        """Modes whose INPUT factor is actually read: with chaining, factor w
+        is replaced by mode w's output before any later mode reads it, so
+        only factors read by an earlier mode (or never recomputed) count."""
+        order = [p.mode for p in self.plans]
+        need = set()
+        for i, d in enumerate(order):
+            for w in range(len(self.shape)):
+                if w == d:
+                    continue
+                if chained and w in order[:i]:
+                    continue
+                need.add(w)
+        return sorted(need)
+
+    def capture(self, factors, chained=True):
+        """CUDA-graph the whole all-mode step (single process only): every
+        memset, tile kernel and carry-tree launch of all modes replays as one
+        graph launch.  Returns the torch.cuda.CUDAGraph."""
+        import torch
+
+        if self.world > 1:
+            raise ValueError("graph capture is for world == 1 (NCCL groups are launched eagerly)")
+        self.run(factors, chained=chained)  # allocate + warm the tables outside capture
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(factors, chained=chained)
+        return g
+
+    def run_host(self, host_factors, host_outputs, dev_factors, chained=True, copy_streams=None):
+        """End-to-end step with HOST buffers (pinned): upload the factors the
+        chain actually reads, run all modes, download every gathered output.
+        Downloads of mode i overlap the compute of mode i+1 on a copy stream.
+        Returns bytes moved (h2d, d2h)."""
+        import torch
+
+        comp = torch.cuda.current_stream(self.device)
+        s_in, s_out = copy_streams or (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
         h2d = d2h = 0
-        for hf, df in zip(host_factors, dev_factors):
-            df.copy_(hf, non_blocking=True)
-            h2d += hf.numel() * hf.element_size()
-        outs = self.run(dev_factors, chained=chained)
-        for ho, o in zip(host_outputs, outs):
-            ho.copy_(o, non_blocking=True)
-            d2h += o.numel() * o.element_size()
+        s_in.wait_stream(comp)
+        with torch.cuda.stream(s_in):
+            for w in self.needed_factors(chained):
+                dev_factors[w].copy_(host_factors[w], non_blocking=True)
+                h2d += host_factors[w].numel() * host_factors[w].element_size()
+        comp.wait_stream(s_in)
+        moved = []
+
+        def download(i, out):
+            s_out.wait_stream(comp)
+            with torch.cuda.stream(s_out):
+                host_outputs[i].copy_(out, non_blocking=True)
+            moved.append(out.numel() * out.element_size())
+
+        self.run(dev_factors, chained=chained, after_mode=download)
+        comp.wait_stream(s_out)
+        d2h = sum(moved)
         return h2d, d2h
 
 

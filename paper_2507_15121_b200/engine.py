@@ -52,7 +52,7 @@ class PlatformConfig:
     accumulation: str = "deterministic-reduce"
     scheduling: str = "dynamic"
     # B200 knobs (defaults keep the reference's fields and meaning intact)
-    tile_nnz: int = 1024        # nonzeros per work-queue tile (a slice of one ISP)
+    tile_nnz: int = 0           # nonzeros per work-queue tile (a slice of one ISP); 0 = auto
     kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
     carry_chunk: int = 256      # carry-tree fan-in
 
@@ -65,8 +65,8 @@ class PlatformConfig:
             raise ValueError(f"accumulation must be one of {ACCUMULATION_MODES}")
         if self.scheduling not in SCHEDULING_MODES:
             raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
-        if self.tile_nnz < 1 or self.carry_chunk < 2:
-            raise ValueError("tile_nnz must be >= 1 and carry_chunk >= 2")
+        if self.tile_nnz < 0 or self.carry_chunk < 2:
+            raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
 
 
 def _torch():
@@ -162,6 +162,23 @@ def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None
 # --------------------------------------------------------- resident tables
 
 
+def auto_tile_nnz(nnz: int, gpu=None) -> int:
+    """Tile size giving every resident warp (~#SM x 24) at least ~8 tiles,
+    clamped to [128, 4096] (a power of two): big tiles amortise the claim and
+    the carries on billion-nonzero modes, small ones keep small modes busy."""
+    torch = _torch()
+    sms = 148
+    try:
+        sms = torch.cuda.get_device_properties(gpu or 0).multi_processor_count
+    except Exception:
+        pass
+    want = max(1, nnz // (sms * 24 * 8))
+    tile = 128
+    while tile * 2 <= want and tile < 4096:
+        tile *= 2
+    return tile
+
+
 class _ShardExec:
     """Device-resident tile table + carry-tree buffers for a set of shards."""
 
@@ -170,7 +187,9 @@ class _ShardExec:
         self.gpu = gpu
         self.rank = rank
         self.det = cfg.accumulation == "deterministic-reduce"
-        tiles, per_shard = tile_table(plan, shard_ids, cfg.tile_nnz)
+        nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(nnz, gpu)
+        tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz)
         self.num_tiles = len(tiles) // 2
         self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
         self.tiles = torch.from_numpy(tiles).to(gpu)

@@ -349,3 +349,40 @@ def test_device_generator_laws():
     # same seed -> same tensor; other seed -> different
     t2 = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3)
     assert np.array_equal(t2.indices, idx)
+
+
+# ------------------------------------------------------------ runner paths
+
+
+def test_runner_graph_and_host_paths(golden):
+    """world == 1 runner: eager, one-graph replay and the host-buffer
+    (pinned, copy-stream overlapped) path give identical chained outputs."""
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    t = tensor_from(golden, "u3")
+    fs = factors_from(golden, "u3", 32, 3)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(isp_capacity=100))
+    runner = DistributedMttkrp(plans, sk.PlatformConfig(rank=32, tile_nnz=64))
+    dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+    eager = [o.clone() for o in runner.run(dev_f)]
+    g = runner.capture(dev_f)
+    for o in runner.outputs:
+        o.fill_(-7.0)
+    g.replay()
+    torch.cuda.synchronize()
+    graphed = [o.clone() for o in runner.outputs]
+    host_f = [torch.from_numpy(f.data.astype(np.float32)).pin_memory() for f in fs]
+    host_o = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in eager]
+    dev_f2 = [torch.zeros_like(f) for f in dev_f]
+    h2d, d2h = runner.run_host(host_f, host_o, dev_f2)
+    torch.cuda.synchronize()
+    assert runner.needed_factors() == [1, 2]
+    assert h2d == sum(host_f[w].numel() * 4 for w in (1, 2))
+    assert d2h == sum(o.numel() * 4 for o in eager)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        assert torch.equal(eager[d], graphed[d])
+        assert torch.equal(eager[d].cpu(), host_o[d])
+        expect = oracle.mttkrp_seq(t.indices, t.values, facs, d)
+        assert rel_err(eager[d].double().cpu().numpy(), expect) <= TOL
+        facs[d] = eager[d].double().cpu().numpy()

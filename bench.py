@@ -223,10 +223,16 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ngpu = torch.cuda.device_count()
+    local_gpu = local % ngpu  # > 1 rank per GPU only for the gloo smoke of the N>1 path
+    torch.cuda.set_device(local_gpu)
+    dev = torch.device("cuda", local_gpu)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -237,7 +243,8 @@ def run_ours(args, cfg):
     modes = list(range(len(shape))) if cfg["modes"] is None else cfg["modes"]
     pcfg = sk.PartitionConfig(devices=world, strategy=cfg["strategy"])
     pl = sk.PlatformConfig(devices=world, rank=R, accumulation=args.accumulation, tile_nnz=args.tile,
-                           kernel_variant=args.variant)
+                           kernel_variant=args.variant, layout=args.layout, l2_budget_mb=args.l2_mb,
+                           max_blocks=args.max_blocks)
 
     t_setup = time.perf_counter()
     if cfg["host_gen"]:
@@ -260,11 +267,11 @@ def run_ours(args, cfg):
     barrier()
 
     # ---- timed region: K all-mode steps, inputs resident in HBM
-    gpu_index = local
+    gpu_index = local_gpu
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         try:
-            gpu_index = int(vis.split(",")[local])
+            gpu_index = int(vis.split(",")[local_gpu])
         except ValueError:
             pass
     clocks = ClockSampler(gpu_index)
@@ -364,6 +371,8 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["desc"], "shape": list(shape), "nnz": nnz, "rank": R,
                        "modes": modes, "partition": f"{cfg['strategy']}, devices={world}, oversub 4, ISP 8192",
                        "accumulation": args.accumulation, "tile_nnz": runner._exec(0, R).tile_nnz,
+                       "layout": [p.layout for p in plans],
+                       "block_shifts": [p.block_shifts for p in plans],
                        "parallelism": f"output-row shards x{world}",
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
@@ -406,8 +415,9 @@ def cpu_mode0(shape, nnz, rank, threads):
 
 def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0):
     """max |gpu - ref| / max(|ref|, 1) over a seeded sample of output rows
-    per mode, ref recomputed in fp64 from the plan's sorted nonzeros with the
-    chained factors (cli.py:247-261 rule)."""
+    per mode, ref recomputed in fp64 from the plan's nonzeros with the
+    chained factors (cli.py:247-261 rule).  Works for any execution layout:
+    the sampled rows' nonzeros are found with a row-membership mask."""
     import torch
 
     facs = [f.data for f in init]
@@ -417,11 +427,14 @@ def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0):
     for i, (p, d) in enumerate(zip(plans, modes)):
         rows = np.sort(rng.choice(p.shape[d], size=min(rows_per_mode, p.shape[d]), replace=False))
         col = p.coords[d]
-        r_t = torch.from_numpy(rows.astype(np.int32)).to(col.device)
-        lo = torch.searchsorted(col, r_t, right=False).cpu().numpy()
-        hi = torch.searchsorted(col, r_t, right=True).cpu().numpy()
-        sel = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)]) if len(rows) else np.zeros(0, np.int64)
-        sel_t = torch.from_numpy(sel).to(col.device)
+        member = torch.zeros(p.shape[d], dtype=torch.bool, device=col.device)
+        member[torch.from_numpy(rows).to(col.device)] = True
+        sel_parts = []
+        chunk = 1 << 27
+        for a in range(0, col.numel(), chunk):
+            m = member[col[a:a + chunk].long()]
+            sel_parts.append(m.nonzero().squeeze(1) + a)
+        sel_t = torch.cat(sel_parts) if sel_parts else torch.zeros(0, dtype=torch.int64, device=col.device)
         idx = np.stack([c.index_select(0, sel_t).cpu().numpy().astype(np.int64) for c in p.coords], 1)
         vals = p.vals.index_select(0, sel_t).cpu().numpy().astype(np.float64)
         contrib = np.repeat(vals[:, None], facs[0].shape[1], axis=1)
@@ -429,9 +442,9 @@ def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0):
             if w != d:
                 contrib *= facs[w][idx[:, w]]
         expect = np.zeros((len(rows), facs[0].shape[1]))
-        pos = np.searchsorted(rows, idx[:, d])
-        np.add.at(expect, pos, contrib)
-        got = outputs[i].index_select(0, r_t.long()).double().cpu().numpy()
+        np.add.at(expect, np.searchsorted(rows, idx[:, d]), contrib)
+        r_t = torch.from_numpy(rows).to(col.device)
+        got = outputs[i].index_select(0, r_t).double().cpu().numpy()
         err = float(np.max(np.abs(got - expect) / np.maximum(np.abs(expect), 1.0))) if len(rows) else 0.0
         worst = max(worst, err)
         checked += len(rows)
@@ -447,8 +460,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--accumulation", default="deterministic-reduce", choices=("deterministic-reduce", "atomic"))
+    ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
+    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "auto"))
+    ap.add_argument("--l2-mb", type=int, default=128)
+    ap.add_argument("--max-blocks", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--parity-rows", type=int, default=512)
     ap.add_argument("--no-parity", action="store_true")

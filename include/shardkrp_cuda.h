@@ -76,6 +76,14 @@ int skrp_stable_sort_by_key(const uint32_t *keys, int64_t n, int key_bits, uint3
                             skrp_stream_t stream);
 int skrp_gather_u32(const uint32_t *src, const uint32_t *perm, int64_t n, uint32_t *dst,
                     skrp_stream_t stream);
+/* Sort keys of the L2-blocked execution layout (B200 addition, no reference
+ * counterpart): key = [shard | c_w >> shifts[w] for every w with shifts[w] >= 0],
+ * widths[w] bits per block id; shard_starts (device, nshards+1 element offsets).
+ * A stable sort by this key reorders nonzeros only inside their shard and
+ * keeps them sorted by c_d inside each block group. */
+int skrp_block_keys(const uint32_t *const *coords, int32_t nmodes, const int32_t *shifts,
+                    const int32_t *widths, const int64_t *shard_starts, int64_t nshards,
+                    int32_t shard_bits, int64_t nnz, uint32_t *keys, skrp_stream_t stream);
 
 /* ------------------------------------------------------------ MTTKRP (K1) */
 typedef struct {

@@ -64,6 +64,7 @@ SIGNATURES = {
     "skrp_sort_workspace_bytes": (sz, [i64, ctypes.c_int]),
     "skrp_stable_sort_by_key": (i32, [vp, i64, ctypes.c_int, vp, vp, vp, sz, vp]),
     "skrp_gather_u32": (i32, [vp, vp, i64, vp, vp]),
+    "skrp_block_keys": (i32, [vp, i32, vp, vp, vp, i64, i32, i64, vp, vp]),
     "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
     "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, vp]),
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),

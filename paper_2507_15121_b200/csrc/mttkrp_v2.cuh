@@ -111,19 +111,52 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         };
 
         for (int64_t base = b0; base < b1; base += 32) {
+            // a short last batch is padded with copies of its last nonzero
+            // carrying value 0: same row (no extra boundary), valid
+            // addresses, zero contribution -- so no per-element predicates
             const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
             const bool lv = lane < nin;
-            const uint32_t r_l = lv ? ld_stream_u32(rowc + base + lane, pol_stream) : 0xffffffffu;
-            const float v_l = lv ? ld_stream_f32(a.values + base + lane, pol_stream) : 0.f;
+            const int64_t src = base + (lv ? lane : nin - 1);
+            const uint32_t r_l = ld_stream_u32(rowc + src, pol_stream);
+            const float v_l = lv ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
             uint32_t c_l[NIN];
 #pragma unroll
-            for (int j = 0; j < NIN; ++j) c_l[j] = lv ? ld_stream_u32(C[j] + base + lane, pol_stream) : 0u;
-            const bool uniform = __all_sync(kFull, !lv || r_l == cur);
+            for (int j = 0; j < NIN; ++j) c_l[j] = ld_stream_u32(C[j] + src, pol_stream);
+            const bool uniform = __all_sync(kFull, r_l == cur);
 
-            // one group of G nonzeros: slot s takes g0 + s*U .. + U-1.
-            // FULL groups carry no per-element predicates.
-            auto group = [&](int g0, auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
+            // Batch classes: 0 = every row is `cur` (registers only);
+            // 1 = exactly one row boundary at e_b (two register accumulators);
+            // 2 = more boundaries (contributions staged in shared memory).
+            int cls = 0, e_b = 32;
+            unsigned cm = 0;
+            float accB[VEC];
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) accB[i] = 0.f;
+            if (!uniform) {
+                const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
+                if (row0 != cur) {  // cur ended with the previous batch
+                    reduce_slots();
+                    write_regs(cur, head, false);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+                    cur = row0;
+                    head = false;
+                }
+                const uint32_t up = __shfl_up_sync(kFull, r_l, 1);
+                cm = __ballot_sync(kFull, lane > 0 && r_l != up);  // rows starting after nonzero 0
+                const int nb = __popc(cm);
+                if (nb == 1) {
+                    cls = 1;
+                    e_b = __ffs(cm) - 1;
+                } else if (nb > 1) {
+                    cls = 2;
+                    reduce_slots();
+                    if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+                }
+            }
+
+            // one group of G nonzeros: slot s takes g0 + s*U .. + U-1
+            auto group = [&](int g0) {
                 float g[U][NIN][VEC];
                 float vv[U];
 #pragma unroll
@@ -133,20 +166,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                        if (FULL || e < nin) ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
+                        ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
                     }
                 }
-                if (uniform) {
+                if (cls == 0) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        if (FULL || g0 + slot * U + u < nin) {
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                float p = vv[u];
+                        for (int i = 0; i < VEC; ++i) {
+                            float p = vv[u];
 #pragma unroll
-                                for (int j = 0; j < NIN - 1; ++j) p *= g[u][j][i];
-                                acc[i] = fmaf(p, g[u][NIN - 1][i], acc[i]);
-                            }
+                            for (int j = 0; j < NIN - 1; ++j) p *= g[u][j][i];
+                            acc[i] = fmaf(p, g[u][NIN - 1][i], acc[i]);
+                        }
+                    }
+                } else if (cls == 1) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const bool inA = g0 + slot * U + u < e_b;
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) {
+                            float p = vv[u];
+#pragma unroll
+                            for (int j = 0; j < NIN - 1; ++j) p *= g[u][j][i];
+                            if (inA) acc[i] = fmaf(p, g[u][NIN - 1][i], acc[i]);
+                            else accB[i] = fmaf(p, g[u][NIN - 1][i], accB[i]);
                         }
                     }
                 } else {
@@ -154,44 +198,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int e = g0 + slot * U + u;
-                        if (FULL || e < nin) {
-                            float p[VEC];
+                        float p[VEC];
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                p[i] = vv[u];
+                        for (int i = 0; i < VEC; ++i) {
+                            p[i] = vv[u];
 #pragma unroll
-                                for (int j = 0; j < NIN; ++j) p[i] *= g[u][j][i];
-                            }
-                            store_vec<VEC>(stage + e * STR + col, p);
+                            for (int j = 0; j < NIN; ++j) p[i] *= g[u][j][i];
                         }
+                        store_vec<VEC>(stage + e * STR + col, p);
                     }
                 }
             };
 
-            bool row0_is_cur = true;
-            unsigned cm = 0;
-            if (!uniform) {
-                const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
-                const uint32_t up = __shfl_up_sync(kFull, r_l, 1);
-                cm = __ballot_sync(kFull, lv && lane > 0 && r_l != up);  // row starts after nonzero 0
-                row0_is_cur = row0 == cur;
+#pragma unroll 1
+            for (int g0 = 0; g0 < nin; g0 += G) group(g0);
+            if (cls == 0) continue;
+            if (cls == 1) {
+                // row cur closed at e_b; the new row continues in registers
                 reduce_slots();
-                if (!row0_is_cur) {
-                    write_regs(cur, head, false);
-                    head = false;
+                write_regs(cur, head, false);
+                head = false;
+                cur = __shfl_sync(kFull, r_l, e_b);
 #pragma unroll
-                    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-                }
-                if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+                for (int i = 0; i < VEC; ++i) acc[i] = accB[i];
+                continue;
             }
-            if (nin == 32) {
-#pragma unroll 1
-                for (int g0 = 0; g0 < 32; g0 += G) group(g0, std::integral_constant<bool, true>{});
-            } else {
-#pragma unroll 1
-                for (int g0 = 0; g0 < nin; g0 += G) group(g0, std::integral_constant<bool, false>{});
-            }
-            if (uniform) continue;
 
             // segmented sums over the staged rows, lanes own columns
             __syncwarp();
@@ -202,8 +233,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                 run[q] = (c < RR) ? carry_row[c] : 0.f;
             }
             // the open row: cur continued by nonzero 0, or the row nonzero 0 opens
-            uint32_t row = row0_is_cur ? cur : __shfl_sync(kFull, r_l, 0);
-            bool rhead = row0_is_cur && head;  // tile head only while the first row is open
+            uint32_t row = cur;  // nonzero 0 continues cur (a closed cur was written above)
+            bool rhead = head;   // tile head only while the first row is open
             for (int e = 0; e < nin; ++e) {
                 if ((cm >> e) & 1u) {
                     write_cols(row, run, rhead);

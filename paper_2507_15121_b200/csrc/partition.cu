@@ -482,3 +482,63 @@ int skrp_gather_u32(const uint32_t *src, const uint32_t *perm, int64_t n, uint32
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- blocked layouts
+// Key of each nonzero for the L2-blocked execution layout (engine.py
+// choose_blocking): [shard | block(c_w1) | block(c_w2) | ...], where
+// block(c) = c >> shift_w.  A stable sort by this key permutes nonzeros only
+// within their shard and keeps them sorted by c_d inside every block group.
+namespace skrp {
+struct BlockKeyArgs {
+    const uint32_t *coords[SKRP_MAX_MODES];
+    int32_t shift[SKRP_MAX_MODES];  // < 0: mode not part of the key
+    int32_t width[SKRP_MAX_MODES];
+};
+
+__global__ void block_keys_kernel(BlockKeyArgs a, int nmodes, const int64_t *__restrict__ shard_starts,
+                                  int64_t nshards, int shard_bits, int64_t nnz, uint32_t *keys)
+{
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+        // shard index: last s with shard_starts[s] <= i
+        int64_t lo = 0, hi = nshards;  // invariant: shard_starts[lo] <= i < shard_starts[hi]
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (shard_starts[mid] <= i) lo = mid; else hi = mid;
+        }
+        uint32_t key = (uint32_t)lo;
+        for (int w = 0; w < nmodes; ++w) {
+            if (a.shift[w] < 0) continue;
+            key = (key << a.width[w]) | (a.coords[w][i] >> a.shift[w]);
+        }
+        (void)shard_bits;
+        keys[i] = key;
+    }
+}
+}  // namespace skrp
+
+extern "C" int skrp_block_keys(const uint32_t *const *coords, int32_t nmodes, const int32_t *shifts,
+                               const int32_t *widths, const int64_t *shard_starts, int64_t nshards,
+                               int32_t shard_bits, int64_t nnz, uint32_t *keys, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(nmodes >= 1 && nmodes <= SKRP_MAX_MODES && nshards >= 1 && nnz >= 0,
+                 "skrp_block_keys: bad sizes");
+    int total = shard_bits;
+    BlockKeyArgs a{};
+    for (int w = 0; w < nmodes; ++w) {
+        a.coords[w] = coords[w];
+        a.shift[w] = shifts[w];
+        a.width[w] = widths[w];
+        if (shifts[w] >= 0) {
+            SKRP_REQUIRE(coords[w] && widths[w] >= 0 && widths[w] <= 31, "skrp_block_keys: bad mode %d", w);
+            total += widths[w];
+        }
+    }
+    SKRP_REQUIRE(total <= 32, "skrp_block_keys: key needs %d > 32 bits", total);
+    if (nnz == 0) return SKRP_OK;
+    SKRP_REQUIRE(shard_starts && keys, "skrp_block_keys: null pointer");
+    block_keys_kernel<<<grid_for(nnz, 256), 256, 0, (cudaStream_t)stream>>>(a, nmodes, shard_starts, nshards,
+                                                                            shard_bits, nnz, keys);
+    SKRP_LAUNCHED("block_keys_kernel");
+    return SKRP_OK;
+}

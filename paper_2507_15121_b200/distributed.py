@@ -23,7 +23,7 @@ from __future__ import annotations
 import numpy as np
 
 from .collective import TransferLedger, allgather_owned_rows
-from .engine import PlatformConfig, _normalize_ranges, _plan_arrays, _shard_exec, assign_shards
+from .engine import PlatformConfig, _normalize_ranges, _plan_arrays, _shard_exec, apply_layout, assign_shards
 
 
 def _dist():
@@ -96,6 +96,7 @@ class DistributedMttkrp:
                         for p in self.plans]
         if self.compute is None:
             for d in range(len(self.plans)):
+                apply_layout(self.plans[d], self.cfg, rank_r, self.mine[d])
                 self._exec(d, rank_r)
 
     def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None,

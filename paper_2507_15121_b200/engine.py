@@ -55,6 +55,9 @@ class PlatformConfig:
     tile_nnz: int = 0           # nonzeros per work-queue tile (a slice of one ISP); 0 = auto
     kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
     carry_chunk: int = 256      # carry-tree fan-in
+    layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked, atomic), "auto"
+    l2_budget_mb: int = 128     # L2 bytes the blocked layout may plan on
+    max_blocks: int = 4         # blocks per input mode the layout search may use (B200-tuned)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -67,6 +70,11 @@ class PlatformConfig:
             raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
+        if self.layout not in ("flycoo", "blocked", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked' or 'auto'")
+        if self.layout == "blocked" and self.accumulation != "atomic":
+            raise ValueError("the blocked layout needs accumulation='atomic' (rows collect "
+                             "contributions from several block groups)")
 
 
 def _torch():
@@ -162,6 +170,97 @@ def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None
 # --------------------------------------------------------- resident tables
 
 
+# ------------------------------------------------------ L2-blocked layouts
+
+_V2_RANKS = (8, 16, 32, 64, 128)
+
+
+def blocking_cost(plan, rank, shifts, shard_ids=None, l2_bytes=96 << 20):
+    """Modelled HBM bytes of one mode in the layout given by `shifts`
+    (shifts[w] >= 0: input mode w cut into blocks of 2^shifts[w] rows).
+
+    stream: nnz*(4N+4).  gathers: if the input blocks of a group fit the L2
+    budget, each group loads them once; otherwise random rows miss with
+    probability 1 - L2/working-set.  output: each group re-reads and rewrites
+    (red) the rows it touches: min(shard rows, group nnz) rows."""
+    n = len(plan.shape)
+    d = plan.mode
+    ids = range(plan.shard_count) if shard_ids is None else shard_ids
+    nnz = sum(plan.shards[j].nnz for j in ids)
+    row_b = rank * 4
+    ws = 0.0
+    groups = 1
+    for w in range(n):
+        if w == d:
+            continue
+        if shifts[w] >= 0:
+            rows = min(plan.shape[w], 1 << shifts[w])
+            groups *= -(-plan.shape[w] // rows)
+        else:
+            rows = plan.shape[w]
+        ws += rows * row_b
+    gathers = 0.0
+    out = 0.0
+    for j in ids:
+        sh = plan.shards[j]
+        if sh.nnz == 0:
+            continue
+        rows = sh.index_range[1] - sh.index_range[0]
+        out += groups * min(rows, sh.nnz / groups) * row_b * (2 if groups > 1 else 1)
+        if ws <= l2_bytes:
+            gathers += groups * ws
+        else:
+            gathers += sh.nnz * (n - 1) * row_b * (1.0 - l2_bytes / ws)
+    return nnz * (4 * n + 4) + gathers + out
+
+
+def choose_blocking(plan, rank, shard_ids=None, l2_bytes=96 << 20, max_blocks=64, force=False):
+    """Block counts (powers of two, up to max_blocks per input mode) that
+    minimise blocking_cost.  Returns (shifts for plan.to_blocked or None,
+    modelled bytes, modelled bytes of the unblocked plan order).
+    force: never return the unblocked layout."""
+    import itertools
+
+    n = len(plan.shape)
+    d = plan.mode
+    ins = [w for w in range(n) if w != d]
+    none = [-1] * n
+    base = blocking_cost(plan, rank, none, shard_ids, l2_bytes)
+    best, best_sh = (float("inf"), None) if force else (base, None)
+    opts = [1 << i for i in range(1, max_blocks.bit_length()) if (1 << i) <= max_blocks]
+    for combo in itertools.product([1] + opts, repeat=len(ins)):
+        if all(b == 1 for b in combo):
+            continue
+        sh = list(none)
+        for w, b in zip(ins, combo):
+            if b > 1 and plan.shape[w] > 1:
+                rows = -(-plan.shape[w] // b)
+                sh[w] = max(0, (rows - 1).bit_length())
+        if all(x < 0 for x in sh):
+            continue
+        c = blocking_cost(plan, rank, sh, shard_ids, l2_bytes)
+        if c < best * 0.999:
+            best, best_sh = c, sh
+    if best_sh is None:
+        return None, base, base
+    return best_sh, best, base
+
+
+def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
+    """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
+    if cfg.layout == "flycoo" or plan.layout != "flycoo":
+        return plan
+    if cfg.accumulation != "atomic" or rank not in _V2_RANKS or len(plan.shape) > 5:
+        if cfg.layout == "blocked":
+            raise ValueError("blocked layout needs atomic accumulation, R in {8,16,32,64,128}, N <= 5")
+        return plan
+    shifts, cost, base = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20,
+                                         max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
+    if shifts is not None and (cfg.layout == "blocked" or cost < 0.8 * base):
+        plan.to_blocked(shifts)
+    return plan
+
+
 def auto_tile_nnz(nnz: int, gpu=None) -> int:
     """Tile size giving every resident warp (~#SM x 24) at least ~8 tiles,
     clamped to [128, 4096] (a power of two): big tiles amortise the claim and
@@ -189,6 +288,9 @@ class _ShardExec:
         self.det = cfg.accumulation == "deterministic-reduce"
         nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(nnz, gpu)
+        if plan.layout == "blocked" and self.det:
+            raise ValueError("blocked layout needs atomic accumulation")
+        self.flags = _lib.FLAG_ADDITIVE if plan.layout == "blocked" else 0
         tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz)
         self.num_tiles = len(tiles) // 2
         self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
@@ -237,6 +339,7 @@ class _ShardExec:
         a.work_counter = self.counter.data_ptr()
         a.persistent_ctas = 0
         a.variant = cfg.kernel_variant
+        a.flags = self.flags
         if events is not None:
             events[0].record()  # current stream == `stream` (callers launch on it)
         _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
@@ -268,7 +371,7 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
 
 
 def _shard_exec(plan, shard_ids, cfg, rank, gpu) -> _ShardExec:
-    key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu))
+    key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout)
     ex = plan._exec_cache.get(key)
     if ex is None:
         ex = _ShardExec(plan, shard_ids, cfg, rank, gpu)
@@ -350,6 +453,7 @@ def mttkrp_mode(plan: ModePartitionPlan, devices: list, cfg: PlatformConfig,
     ledger = ledger if ledger is not None else TransferLedger()
     if assignment is None:
         assignment = assign_shards(plan, m, cfg.scheduling)
+    apply_layout(plan, cfg, rank)
 
     events = []
     for dev in devices:

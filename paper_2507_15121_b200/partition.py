@@ -139,6 +139,11 @@ class ModePartitionPlan:
         self._host_idx = None
         self._host_vals = None
         self._exec_cache = {}
+        # execution layout of the device arrays: "flycoo" (plan order) or
+        # "blocked" (see to_blocked); groups: per shard, [start, stop) ranges
+        self.layout = "flycoo"
+        self.block_shifts = None
+        self.groups = None
         self.shards = [
             TensorShard(self, mode, j, (int(self.bounds[j]), int(self.bounds[j + 1])),
                         int(self.offsets[j]), int(self.offsets[j + 1]),
@@ -191,7 +196,8 @@ class ModePartitionPlan:
                 self._host_idx = src._indices[self.order()]
             else:
                 import torch
-                self._host_idx = torch.stack(self.coords, 1).cpu().numpy().astype(INDEX_DTYPE)
+                arr = torch.stack(self.coords, 1).cpu().numpy().astype(INDEX_DTYPE)
+                self._host_idx = self._to_plan_order(arr)
             self._host_idx.setflags(write=False)
         return self._host_idx
 
@@ -202,9 +208,93 @@ class ModePartitionPlan:
             if src is not None and src._values is not None and self.perm is not None:
                 self._host_vals = src._values[self.order()]
             else:
-                self._host_vals = self.vals.cpu().numpy()
+                self._host_vals = self._to_plan_order(self.vals.cpu().numpy())
             self._host_vals.setflags(write=False)
         return self._host_vals
+
+    def _to_plan_order(self, arr):
+        if self.layout == "flycoo":
+            return arr
+        if getattr(self, "exec_perm", None) is None:
+            raise ValueError("blocked plan built without its permutation: host views unavailable")
+        out = np.empty_like(arr)
+        out[self.exec_perm.cpu().numpy().astype(np.int64)] = arr
+        return out
+
+    def to_blocked(self, shifts):
+        """Reorder the device arrays IN PLACE into the L2-blocked execution
+        layout: inside every shard, nonzeros are grouped by the blocks
+        (c_w >> shifts[w]) of the blocked input modes and stay sorted by c_d
+        inside each group (stable sort by [shard | blocks]).  Shard offsets are
+        unchanged; the host-visible plan (``_indices``, ``_values``, ISPs) keeps
+        the reference order (it is derived from the source tensor + order).
+        The per-mode factor rows touched by one group then fit in L2."""
+        import torch
+
+        if self.layout != "flycoo":
+            raise ValueError("plan is already in a blocked layout")
+        n = len(self.shape)
+        shifts = [int(x) for x in shifts]
+        if len(shifts) != n or shifts[self.mode] >= 0:
+            raise ValueError("need one shift per mode, and none for the output mode")
+        if all(x < 0 for x in shifts):
+            return self
+        if self._host_idx is None and self._source is not None and self.perm is not None:
+            pass  # host views stay derivable from source + order
+        widths = [0] * n
+        for w in range(n):
+            if shifts[w] >= 0:
+                widths[w] = max(1, _key_bits(-(-self.shape[w] // (1 << shifts[w]))))
+        k = self.shard_count
+        shard_bits = max(1, _key_bits(k))
+        total_bits = shard_bits + sum(widths)
+        if total_bits > 32:
+            raise ValueError(f"blocked key needs {total_bits} > 32 bits")
+        nnz = self.nnz
+        dev = self.vals.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        starts = torch.from_numpy(np.ascontiguousarray(self.offsets)).to(dev)
+        keys = torch.empty(nnz, dtype=torch.int32, device=dev)
+        cptr = (_lib.vp * n)(*[c.data_ptr() for c in self.coords])
+        sh = np.ascontiguousarray(shifts, dtype=np.int32)
+        wd = np.ascontiguousarray(widths, dtype=np.int32)
+        _lib.call("skrp_block_keys", cptr, n, sh.ctypes.data, wd.ctypes.data, starts.data_ptr(), k, shard_bits,
+                  nnz, keys.data_ptr(), stream)
+        sorted_keys = torch.empty_like(keys)
+        perm = torch.empty_like(keys)
+        ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, total_bits)
+        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+        _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), nnz, total_bits, sorted_keys.data_ptr(),
+                  perm.data_ptr(), ws.data_ptr(), ws_bytes, stream)
+        del ws, keys
+        # group sizes: histogram of the sorted keys (bins = 2^total_bits)
+        counts = torch.empty(1 << total_bits, dtype=torch.int64, device=dev)
+        _lib.call("skrp_histogram", sorted_keys.data_ptr(), nnz, 1 << total_bits, counts.data_ptr(), stream)
+        del sorted_keys
+        for w in range(n):
+            out = torch.empty_like(self.coords[w])
+            _lib.call("skrp_gather_u32", self.coords[w].data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
+            self.coords[w] = out
+        out = torch.empty_like(self.vals)
+        _lib.call("skrp_gather_u32", self.vals.data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
+        self.vals = out
+        # device position i holds plan-order element exec_perm[i] (kept only when
+        # the plan keeps its permutation, i.e. host views are wanted)
+        self.exec_perm = perm if self.perm is not None else None
+        c = counts.cpu().numpy()
+        per_shard = 1 << (total_bits - shard_bits)
+        self.groups = []
+        for j in range(k):
+            cnt = c[j * per_shard:(j + 1) * per_shard]
+            ends = self.offsets[j] + np.cumsum(cnt)
+            begins = ends - cnt
+            keep = cnt > 0
+            self.groups.append(np.stack([begins[keep], ends[keep]], axis=1).astype(np.int64))
+        self.layout = "blocked"
+        self.block_shifts = shifts
+        self._exec_cache.clear()
+        torch.cuda.current_stream(dev).synchronize()
+        return self
 
     def release_device(self):
         self.coords = self.vals = self.perm = None
@@ -309,14 +399,21 @@ def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
     cap = plan.isp_capacity
     step = max(1, min(tile_nnz, cap))
     starts, stops, per_shard = [], [], []
+    blocked = getattr(plan, "layout", "flycoo") == "blocked"
     for j in shard_ids:
         sh = plan.shards[j]
         n = sh.nnz
         if n == 0:
             per_shard.append(0)
             continue
-        isp0 = np.arange(0, n, cap, dtype=np.int64)
-        isp1 = np.minimum(isp0 + cap, n)
+        if blocked:
+            # blocked layout: tiles slice the shard's block groups instead
+            g = plan.groups[j]
+            isp0 = g[:, 0] - sh.start
+            isp1 = g[:, 1] - sh.start
+        else:
+            isp0 = np.arange(0, n, cap, dtype=np.int64)
+            isp1 = np.minimum(isp0 + cap, n)
         pieces = (isp1 - isp0 + step - 1) // step
         total = int(pieces.sum())
         first = np.repeat(np.cumsum(pieces) - pieces, pieces)

@@ -386,3 +386,52 @@ def test_runner_graph_and_host_paths(golden):
         expect = oracle.mttkrp_seq(t.indices, t.values, facs, d)
         assert rel_err(eager[d].double().cpu().numpy(), expect) <= TOL
         facs[d] = eager[d].double().cpu().numpy()
+
+
+# ---------------------------------------------------------- blocked layout
+
+
+@pytest.mark.parametrize("name", ["u3", "z3", "z4", "u5"])
+def test_blocked_layout_parity(golden, name):
+    """L2-blocked execution layout (atomic, additive flushes): same outputs
+    within tolerance, shard ranges unchanged, host plan views still bit-exact."""
+    from paper_2507_15121_b200.engine import choose_blocking
+
+    t = tensor_from(golden, name)
+    fs = factors_from(golden, name, 32, t.num_modes)
+    ref = golden("mttkrp.npz")
+    plans = golden("plans.npz")
+    for d in range(t.num_modes):
+        p = sk.build_mode_plan(t, d, sk.PartitionConfig(devices=2))
+        shards_before = [(s_.start, s_.stop, s_.index_range) for s_ in p.shards]
+        shifts, _, _ = choose_blocking(p, 32, l2_bytes=1 << 10)  # tiny budget: force blocking
+        shifts = shifts or [(-1 if w == d else 1) for w in range(t.num_modes)]
+        p.to_blocked(shifts)
+        assert p.layout == "blocked"
+        assert [(s_.start, s_.stop, s_.index_range) for s_ in p.shards] == shards_before
+        # every group lies inside its shard and groups tile the shard
+        for s_, g in zip(p.shards, p.groups):
+            if s_.nnz:
+                assert g[0, 0] == s_.start and g[-1, 1] == s_.stop and np.all(g[1:, 0] == g[:-1, 1])
+        assert np.array_equal(p._indices, plans[f"{name}_m{d}_sorted_indices"])
+        cfg = sk.PlatformConfig(devices=2, rank=32, accumulation="atomic", tile_nnz=16, layout="blocked")
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+        assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL
+
+
+def test_blocked_layout_through_runner(golden):
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    t = sk.synth_tensor((400, 300, 200), 300_000, seed=5)
+    fs = sk.random_factors(t.shape, 32, seed=2)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(), keep_permutation=False)
+    cfg = sk.PlatformConfig(rank=32, accumulation="atomic", layout="blocked", l2_budget_mb=0)
+    runner = DistributedMttkrp(plans, cfg)
+    dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+    outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+    assert all(p.layout == "blocked" for p in plans)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(outs[d], expect) <= TOL
+        facs[d] = outs[d]

@@ -258,6 +258,9 @@ def run_ours(args, cfg):
     init = sk.random_factors(shape, R, seed=0)
     host_f = [torch.from_numpy(f.data.astype(np.float32)).pin_memory() for f in init]
     dev_f = [h.to(dev) for h in host_f]
+    if args.shifts:
+        for p_, sh in zip(plans, args.shifts.split(";")):
+            p_.to_blocked([int(x) for x in sh.split(",")])
     runner = DistributedMttkrp(plans, pl, rank=rank, world=world, device=dev)
     runner.prepare(R)
     setup_s = time.perf_counter() - t_setup
@@ -463,8 +466,9 @@ def main():
     ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
     ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "auto"))
-    ap.add_argument("--l2-mb", type=int, default=128)
+    ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=4)
+    ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--parity-rows", type=int, default=512)
     ap.add_argument("--no-parity", action="store_true")

@@ -56,7 +56,7 @@ class PlatformConfig:
     kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
     carry_chunk: int = 256      # carry-tree fan-in
     layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked, atomic), "auto"
-    l2_budget_mb: int = 128     # L2 bytes the blocked layout may plan on
+    l2_budget_mb: int = 192     # L2 bytes the blocked layout plans on (B200-calibrated)
     max_blocks: int = 4         # blocks per input mode the layout search may use (B200-tuned)
 
     def __post_init__(self):

@@ -289,7 +289,8 @@ class ModePartitionPlan:
             ends = self.offsets[j] + np.cumsum(cnt)
             begins = ends - cnt
             keep = cnt > 0
-            self.groups.append(np.stack([begins[keep], ends[keep]], axis=1).astype(np.int64))
+            gkey = np.arange(per_shard, dtype=np.int64)[keep]  # block-tuple id of each group
+            self.groups.append(np.stack([begins[keep], ends[keep], gkey], axis=1).astype(np.int64))
         self.layout = "blocked"
         self.block_shifts = shifts
         self._exec_cache.clear()
@@ -427,6 +428,21 @@ def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
         e = np.concatenate(stops)
     else:
         s = e = np.zeros(0, dtype=np.int64)
+    if blocked and len(s):
+        # work-queue order: block tuple major, shard minor -- every shard's
+        # group of the same factor blocks runs back to back, so a block pair
+        # is loaded into L2 once per device instead of once per shard
+        gkeys = []
+        for j in shard_ids:
+            sh = plan.shards[j]
+            if sh.nnz == 0:
+                continue
+            g = plan.groups[j]
+            glen = ((g[:, 1] - g[:, 0]) + step - 1) // step
+            gkeys.append(np.repeat(g[:, 2], glen))
+        gk = np.concatenate(gkeys)
+        order = np.argsort(gk, kind="stable")
+        s, e = s[order], e[order]
     tiles = np.empty(2 * len(s), dtype=np.int64)
     tiles[0::2] = s
     tiles[1::2] = e

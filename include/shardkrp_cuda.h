@@ -130,12 +130,18 @@ int skrp_mttkrp_host(const uint64_t *indices, const double *values, int64_t nnz,
                      int32_t mode, double *out, int32_t device);
 
 /* -------------------------------------------------------- synthetic (K7) */
+/* element i of a batch uses counter offset + i of the (seed, stream_id) stream */
 int skrp_synth_uniform_coords(int32_t *out, int64_t n, int64_t size, uint64_t seed,
-                              int32_t stream_id, skrp_stream_t stream);
+                              int32_t stream_id, int64_t offset, skrp_stream_t stream);
 int skrp_synth_zipf_coords(int32_t *out, int64_t n, const double *cdf, int64_t size,
-                           uint64_t seed, int32_t stream_id, skrp_stream_t stream);
+                           uint64_t seed, int32_t stream_id, int64_t offset, skrp_stream_t stream);
 int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed,
                       skrp_stream_t stream);
+/* keep[i] = 1 iff element i is the first occurrence of its coordinate tuple
+ * (synth.py:68-84 dedup rule).  table: caller scratch of table_slots uint64
+ * (power of two >= 2n). */
+int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int64_t n, void *table,
+                    int64_t table_slots, uint8_t *keep, skrp_stream_t stream);
 
 /* ---------------------------------------------------------- CP-ALS (K6) */
 int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_stream_t stream);
@@ -148,6 +154,12 @@ int skrp_scale_cols(float *x, int64_t rows, int32_t rank, const double *scale,
 int skrp_model_inner(const uint32_t *const *coords, const float *values, int64_t nnz,
                      int32_t nmodes, const float *const *factors, const double *lambdas,
                      int32_t rank, double *out, skrp_stream_t stream);
+/* out[0] = sum_i sum_r lambdas[r] a[i,r] b[i,r]: <X, Xhat> from the last mode's
+ * MTTKRP output b and updated factor a (the fit without a pass over nnz). */
+int skrp_weighted_dot(const float *a, const float *b, int64_t rows, int32_t rank,
+                      const double *lambdas, double *out, skrp_stream_t stream);
+/* out[0] = sum v^2 (||X||^2). */
+int skrp_sumsq(const float *v, int64_t n, double *out, skrp_stream_t stream);
 
 #ifdef __cplusplus
 }

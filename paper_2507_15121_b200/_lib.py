@@ -68,14 +68,17 @@ SIGNATURES = {
     "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
     "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, vp]),
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),
-    "skrp_synth_uniform_coords": (i32, [vp, i64, i64, u64, i32, vp]),
-    "skrp_synth_zipf_coords": (i32, [vp, i64, vp, i64, u64, i32, vp]),
+    "skrp_synth_uniform_coords": (i32, [vp, i64, i64, u64, i32, i64, vp]),
+    "skrp_synth_zipf_coords": (i32, [vp, i64, vp, i64, u64, i32, i64, vp]),
     "skrp_synth_values": (i32, [vp, i64, i32, u64, vp]),
+    "skrp_dedup_mark": (i32, [vp, i32, i64, vp, i64, vp, vp]),
     "skrp_gram": (i32, [vp, i64, i32, vp, vp]),
     "skrp_apply_rr": (i32, [vp, i64, i32, vp, vp, vp]),
     "skrp_col_sumsq": (i32, [vp, i64, i32, vp, vp]),
     "skrp_scale_cols": (i32, [vp, i64, i32, vp, vp]),
     "skrp_model_inner": (i32, [vp, vp, i64, i32, vp, vp, i32, vp, vp]),
+    "skrp_weighted_dot": (i32, [vp, vp, i64, i32, vp, vp, vp]),
+    "skrp_sumsq": (i32, [vp, i64, vp, vp]),
 }
 
 _LIB = None

@@ -143,6 +143,30 @@ def _device_inner(tensor: SparseTensorCOO, dev_factors, lambdas):
     return float(inner), float(sq)
 
 
+def _fused_inner(new, m_out, lambdas) -> float:
+    """<X, Xhat> = sum_r lambda_r sum_i F_last[i, r] M_last[i, r]: the last
+    mode's MTTKRP output already holds sum over its nonzeros of
+    v * prod_{w < last} F_w, so the fit needs no pass over the nonzeros."""
+    import torch
+
+    rows, rank = new.shape
+    lam = torch.from_numpy(np.ascontiguousarray(lambdas, dtype=np.float64)).to(new.device)
+    out = torch.empty(1, dtype=torch.float64, device=new.device)
+    _lib.call("skrp_weighted_dot", new.data_ptr(), m_out.data_ptr(), rows, rank, lam.data_ptr(), out.data_ptr(),
+              torch.cuda.current_stream(new.device).cuda_stream)
+    return float(out.item())
+
+
+def _device_sumsq(tensor) -> float:
+    import torch
+
+    _, vals = tensor.device_arrays()
+    out = torch.empty(1, dtype=torch.float64, device=vals.device)
+    _lib.call("skrp_sumsq", vals.data_ptr(), tensor.nnz, out.data_ptr(),
+              torch.cuda.current_stream(vals.device).cuda_stream)
+    return float(out.item())
+
+
 def _fit_value(x_sq, inner, grams, lambdas):
     if x_sq == 0.0:
         raise ValueError("tensor has zero Frobenius norm; fit undefined")
@@ -198,6 +222,7 @@ def cp_als(tensor: SparseTensorCOO, rank: int, iterations: int, platform: Platfo
     grams = [_gram_device(f) for f in cur]
     lambdas = np.ones(rank)
     history = []
+    x_sq = None
     for _ in range(iterations):
         for d in range(tensor.num_modes):
             if mttkrp_impl == "engine":
@@ -206,12 +231,15 @@ def cp_als(tensor: SparseTensorCOO, rank: int, iterations: int, platform: Platfo
             else:
                 m_out = mttkrp(tensor, cur, d, as_numpy=False)
             new, lambdas = _als_update_device(m_out, [grams[w] for w in range(tensor.num_modes) if w != d])
+            if d == tensor.num_modes - 1:
+                inner = _fused_inner(new, m_out, lambdas)
             cur[d] = new
             grams[d] = _gram_device(new)
             for dev in devices:
                 dev.factors[d] = new if new.device == dev.cuda_device else new.to(dev.cuda_device)
-        inner, sq = _device_inner(tensor, cur, lambdas)
-        history.append(_fit_value(_x_sq(tensor, sq), inner, grams, lambdas))
+        if x_sq is None:
+            x_sq = _x_sq(tensor, None) if tensor._values is not None else _device_sumsq(tensor)
+        history.append(_fit_value(x_sq, inner, grams, lambdas))
         if fit_tol is not None and len(history) > 1 and history[-1] - history[-2] < fit_tol:
             break
     factors = [FactorMatrix(w, f.double().cpu().numpy()) for w, f in enumerate(cur)]

@@ -13,81 +13,155 @@
 
 namespace skrp {
 
-constexpr int kGramRows = 32;
+// Y^T Y: a 256-thread block owns a chunk of rows; threads hold a TSxTS tile
+// of the R x R output in fp32 over the chunk (<= kGramChunk rows, so fp32
+// partial sums stay accurate), then add it into the fp64 result atomically.
+constexpr int kGramChunk = 1024;
+constexpr int kGramTileRows = 64;
 
-__global__ void __launch_bounds__(256) gram_kernel(const float *__restrict__ y, int64_t rows, int R,
-                                                   double *g)
+template <int R>
+__global__ void __launch_bounds__(256) gram_tiled_kernel(const float *__restrict__ y, int64_t rows, double *g)
 {
-    extern __shared__ float ys[];  // kGramRows x R
-    const int pairs = R * R;
-    const int per = (pairs + 255) / 256;
-    double acc[16];
+    constexpr int TS = (R * R + 255) / 256 >= 16 ? 4 : ((R * R + 255) / 256 >= 4 ? 2 : 1);
+    constexpr int TPR = R / TS;  // threads per output row-strip
+    __shared__ float ys[kGramTileRows][R + 1];
+    const int tid = threadIdx.x;
+    const int ti = tid / TPR, tj = tid % TPR;  // output tile (ti*TS.., tj*TS..)
+    const bool active = ti < TPR;
+    double dacc[TS][TS];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-    for (int64_t r0 = (int64_t)blockIdx.x * kGramRows; r0 < rows; r0 += (int64_t)gridDim.x * kGramRows) {
-        int nr = (int)std::min<int64_t>(kGramRows, rows - r0);
-        for (int i = threadIdx.x; i < nr * R; i += 256) ys[i] = y[r0 * R + i];
-        __syncthreads();
+    for (int a = 0; a < TS; ++a)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (j >= per) break;
-            int pq = threadIdx.x + 256 * j;
-            if (pq >= pairs) break;
-            int p = pq / R, q = pq % R;
-            double s = 0.0;
-            for (int r = 0; r < nr; ++r) s += (double)ys[r * R + p] * (double)ys[r * R + q];
-            acc[j] += s;
-        }
-        __syncthreads();
-    }
+        for (int b = 0; b < TS; ++b) dacc[a][b] = 0.0;
+    for (int64_t c0 = (int64_t)blockIdx.x * kGramChunk; c0 < rows; c0 += (int64_t)gridDim.x * kGramChunk) {
+        float acc[TS][TS];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (j >= per) break;
-        int pq = threadIdx.x + 256 * j;
-        if (pq < pairs) atomicAdd(&g[pq], acc[j]);
-    }
-}
-
-// out[i, :] = m[i, :] @ w   (w: R x R fp64, row-major)
-__global__ void __launch_bounds__(256) apply_rr_kernel(const float *__restrict__ m, int64_t rows, int R,
-                                                       const double *__restrict__ w, float *out)
-{
-    extern __shared__ double ws[];
-    for (int i = threadIdx.x; i < R * R; i += 256) ws[i] = w[i];
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * 256) >> 5;
-    const int nchunk = (R + 31) / 32;  // R <= 256 -> <= 8
-    for (int64_t i = warp; i < rows; i += nwarps) {
-        double acc[8];
-        float mv[8];
+        for (int a = 0; a < TS; ++a)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            acc[j] = 0.0;
-            int c = lane + 32 * j;
-            mv[j] = (j < nchunk && c < R) ? m[i * R + c] : 0.f;
-        }
+            for (int b = 0; b < TS; ++b) acc[a][b] = 0.f;
+        const int64_t c1 = c0 + kGramChunk < rows ? c0 + kGramChunk : rows;
+        for (int64_t r0 = c0; r0 < c1; r0 += kGramTileRows) {
+            const int nr = (int)((c1 - r0) < kGramTileRows ? (c1 - r0) : kGramTileRows);
+            __syncthreads();
+            for (int i = tid; i < kGramTileRows * R; i += 256) {
+                const int rr = i / R, cc = i % R;
+                ys[rr][cc] = rr < nr ? y[(r0 + rr) * R + cc] : 0.f;
+            }
+            __syncthreads();
+            if (active) {
+#pragma unroll 4
+                for (int rr = 0; rr < kGramTileRows; ++rr) {
+                    float a_[TS], b_[TS];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (j >= nchunk) break;
-            for (int l = 0; l < 32; ++l) {
-                int k = 32 * j + l;
-                if (k >= R) break;
-                double mk = (double)__shfl_sync(0xffffffffu, mv[j], l);
+                    for (int a = 0; a < TS; ++a) a_[a] = ys[rr][ti * TS + a];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    int c = lane + 32 * q;
-                    if (q < nchunk && c < R) acc[q] += mk * ws[k * R + c];
+                    for (int b = 0; b < TS; ++b) b_[b] = ys[rr][tj * TS + b];
+#pragma unroll
+                    for (int a = 0; a < TS; ++a)
+#pragma unroll
+                        for (int b = 0; b < TS; ++b) acc[a][b] = fmaf(a_[a], b_[b], acc[a][b]);
                 }
             }
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            int c = lane + 32 * q;
-            if (q < nchunk && c < R) out[i * R + c] = (float)acc[q];
+        for (int a = 0; a < TS; ++a)
+#pragma unroll
+            for (int b = 0; b < TS; ++b) dacc[a][b] += (double)acc[a][b];
+    }
+    if (active) {
+#pragma unroll
+        for (int a = 0; a < TS; ++a)
+#pragma unroll
+            for (int b = 0; b < TS; ++b) atomicAdd(&g[(ti * TS + a) * R + tj * TS + b], dacc[a][b]);
+    }
+}
+
+// generic fallback (any R <= 64): one thread per (p, q) pair, fp64 sums
+__global__ void __launch_bounds__(256) gram_generic_kernel(const float *__restrict__ y, int64_t rows, int R,
+                                                           double *g)
+{
+    const int pairs = R * R;
+    for (int pq = threadIdx.x; pq < pairs; pq += 256) {
+        const int p = pq / R, q = pq % R;
+        double s = 0.0;
+        for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) s += (double)y[r * R + p] * (double)y[r * R + q];
+        atomicAdd(&g[pq], s);
+    }
+}
+
+// out[i, :] = m[i, :] @ w (w: R x R, fp64 on input, used in fp32): a block
+// handles 32 rows; thread (row, column group of R/8) keeps R/8 accumulators.
+template <int R>
+__global__ void __launch_bounds__(256) apply_rr_tiled_kernel(const float *__restrict__ m, int64_t rows,
+                                                             const double *__restrict__ w, float *out)
+{
+    constexpr int CG = R / 8;  // columns per thread
+    __shared__ float ws[R][R];
+    __shared__ float ms[32][R + 1];
+    for (int i = threadIdx.x; i < R * R; i += 256) ws[i / R][i % R] = (float)w[i];
+    const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
+    for (int64_t r0 = (int64_t)blockIdx.x * 32; r0 < rows; r0 += (int64_t)gridDim.x * 32) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 32 * R; i += 256) {
+            const int rr = i / R, cc = i % R;
+            ms[rr][cc] = (r0 + rr < rows) ? m[(r0 + rr) * R + cc] : 0.f;
+        }
+        __syncthreads();
+        float acc[CG];
+#pragma unroll
+        for (int c = 0; c < CG; ++c) acc[c] = 0.f;
+#pragma unroll 8
+        for (int k = 0; k < R; ++k) {
+            const float a = ms[r][k];
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc[c] = fmaf(a, ws[k][cg * CG + c], acc[c]);
+        }
+        if (r0 + r < rows) {
+#pragma unroll
+            for (int c = 0; c < CG; ++c) out[(r0 + r) * R + cg * CG + c] = acc[c];
         }
     }
+}
+
+// generic fallback: warp per row, lanes over columns, fp64 accumulation
+__global__ void __launch_bounds__(256) apply_rr_kernel(const float *__restrict__ m, int64_t rows, int R,
+                                                       const double *__restrict__ w, float *out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * 256) >> 5;
+    for (int64_t i = warp; i < rows; i += nwarps) {
+        for (int c = lane; c < R; c += 32) {
+            double acc = 0.0;
+            for (int k = 0; k < R; ++k) acc += (double)m[i * R + k] * w[k * R + c];
+            out[i * R + c] = (float)acc;
+        }
+    }
+}
+
+// sum_i sum_r lambda_r a[i, r] b[i, r]  (the fit's <X, Xhat> from the last
+// mode's MTTKRP output, cpd.py:84-105 identity; fp64 accumulation)
+__global__ void __launch_bounds__(256) weighted_dot_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                                           int64_t rows, int R, const double *__restrict__ lam,
+                                                           double *out)
+{
+    double s = 0.0;
+    const int64_t n = rows * R;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+        s += lam[i % R] * (double)a[i] * (double)b[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+__global__ void __launch_bounds__(256) sumsq_kernel(const float *__restrict__ v, int64_t n, double *out)
+{
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+        s += (double)v[i] * (double)v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
 }
 
 __global__ void __launch_bounds__(256) col_sumsq_kernel(const float *__restrict__ x, int64_t rows, int R,
@@ -176,8 +250,13 @@ int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_st
     SKRP_CUDA(cudaMemsetAsync(g_out, 0, sizeof(double) * rank * rank, s));
     if (rows == 0) return SKRP_OK;
     SKRP_REQUIRE(y, "skrp_gram: null input");
-    gram_kernel<<<grid_cap((rows + kGramRows - 1) / kGramRows, 4), 256, sizeof(float) * kGramRows * rank, s>>>(
-        y, rows, rank, g_out);
+    unsigned grid = grid_cap((rows + kGramChunk - 1) / kGramChunk, 8);
+    switch (rank) {
+    case 64: gram_tiled_kernel<64><<<grid, 256, 0, s>>>(y, rows, g_out); break;
+    case 32: gram_tiled_kernel<32><<<grid, 256, 0, s>>>(y, rows, g_out); break;
+    case 16: gram_tiled_kernel<16><<<grid, 256, 0, s>>>(y, rows, g_out); break;
+    default: gram_generic_kernel<<<grid_cap(rows, 4), 256, 0, s>>>(y, rows, rank, g_out); break;
+    }
     SKRP_LAUNCHED("gram_kernel");
     return SKRP_OK;
 }
@@ -188,11 +267,41 @@ int skrp_apply_rr(const float *m, int64_t rows, int32_t rank, const double *w, f
     SKRP_REQUIRE(rank >= 1 && rank <= 64 && rows >= 0, "skrp_apply_rr: rank in [1,64]");
     if (rows == 0) return SKRP_OK;
     SKRP_REQUIRE(m && w && out && m != out, "skrp_apply_rr: bad pointers (in-place not allowed)");
-    size_t smem = sizeof(double) * rank * rank;
-    if (smem > 48 * 1024)
-        SKRP_CUDA(cudaFuncSetAttribute(apply_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    apply_rr_kernel<<<grid_cap((rows + 7) / 8, 8), 256, smem, (cudaStream_t)stream>>>(m, rows, rank, w, out);
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned grid = grid_cap((rows + 31) / 32, 8);
+    switch (rank) {
+    case 64: apply_rr_tiled_kernel<64><<<grid, 256, 0, s>>>(m, rows, w, out); break;
+    case 32: apply_rr_tiled_kernel<32><<<grid, 256, 0, s>>>(m, rows, w, out); break;
+    case 16: apply_rr_tiled_kernel<16><<<grid, 256, 0, s>>>(m, rows, w, out); break;
+    case 8: apply_rr_tiled_kernel<8><<<grid, 256, 0, s>>>(m, rows, w, out); break;
+    default: apply_rr_kernel<<<grid_cap((rows + 7) / 8, 8), 256, 0, s>>>(m, rows, rank, w, out); break;
+    }
     SKRP_LAUNCHED("apply_rr_kernel");
+    return SKRP_OK;
+}
+
+int skrp_weighted_dot(const float *a, const float *b, int64_t rows, int32_t rank, const double *lambdas,
+                      double *out, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(rank >= 1 && rows >= 0 && out, "skrp_weighted_dot: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    SKRP_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+    if (rows == 0) return SKRP_OK;
+    SKRP_REQUIRE(a && b && lambdas, "skrp_weighted_dot: null pointer");
+    weighted_dot_kernel<<<grid_cap((rows * rank + 255) / 256, 8), 256, 0, s>>>(a, b, rows, rank, lambdas, out);
+    SKRP_LAUNCHED("weighted_dot_kernel");
+    return SKRP_OK;
+}
+
+int skrp_sumsq(const float *v, int64_t n, double *out, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(n >= 0 && out, "skrp_sumsq: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    SKRP_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+    if (n == 0) return SKRP_OK;
+    SKRP_REQUIRE(v, "skrp_sumsq: null pointer");
+    sumsq_kernel<<<grid_cap((n + 255) / 256, 8), 256, 0, s>>>(v, n, out);
+    SKRP_LAUNCHED("sumsq_kernel");
     return SKRP_OK;
 }
 

@@ -19,43 +19,36 @@ __device__ __forceinline__ double u53(uint32_t hi, uint32_t lo)
     return (double)(bits & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0);
 }
 
-__global__ void uniform_coords_kernel(int32_t *out, int64_t n, uint64_t size, uint64_t seed, uint32_t sid)
+// element i's draw uses Philox counter (offset + i): batches drawn with
+// consecutive offsets continue one stream (the dedup top-up rounds)
+__global__ void uniform_coords_kernel(int32_t *out, int64_t n, uint64_t size, uint64_t seed, uint32_t sid,
+                                      int64_t offset)
 {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t groups = (n + 3) / 4;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < groups; q += stride) {
-        Philox4 r = philox4x32_10((uint32_t)q, (uint32_t)(q >> 32), sid, 0x5EED0001u, (uint32_t)seed,
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t g = (uint64_t)(offset + i);
+        Philox4 r = philox4x32_10((uint32_t)g, (uint32_t)(g >> 32), sid, 0x5EED0001u, (uint32_t)seed,
                                   (uint32_t)(seed >> 32));
-        uint32_t v[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            int64_t i = 4 * q + j;
-            if (i < n) out[i] = (int32_t)(((uint64_t)v[j] * size) >> 32);
-        }
+        out[i] = (int32_t)(((uint64_t)r.x * size) >> 32);
     }
 }
 
 __global__ void zipf_coords_kernel(int32_t *out, int64_t n, const double *__restrict__ cdf, int64_t size,
-                                   uint64_t seed, uint32_t sid)
+                                   uint64_t seed, uint32_t sid, int64_t offset)
 {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t pairs = (n + 1) / 2;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < pairs; q += stride) {
-        Philox4 r = philox4x32_10((uint32_t)q, (uint32_t)(q >> 32), sid, 0x5EED0002u, (uint32_t)seed,
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t g = (uint64_t)(offset + i);
+        Philox4 r = philox4x32_10((uint32_t)g, (uint32_t)(g >> 32), sid, 0x5EED0002u, (uint32_t)seed,
                                   (uint32_t)(seed >> 32));
-        double u[2] = {u53(r.x, r.y), u53(r.z, r.w)};
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            int64_t i = 2 * q + j;
-            if (i >= n) break;
-            // first index with cdf[idx] >= u  (np.searchsorted, side="left")
-            int64_t lo = 0, hi = size;
-            while (lo < hi) {
-                int64_t mid = (lo + hi) >> 1;
-                if (cdf[mid] < u[j]) lo = mid + 1; else hi = mid;
-            }
-            out[i] = (int32_t)(lo < size ? lo : size - 1);
+        const double u = u53(r.x, r.y);
+        // first index with cdf[idx] >= u  (np.searchsorted, side="left")
+        int64_t lo = 0, hi = size;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (cdf[mid] < u) lo = mid + 1; else hi = mid;
         }
+        out[i] = (int32_t)(lo < size ? lo : size - 1);
     }
 }
 
@@ -93,25 +86,25 @@ using namespace skrp;
 extern "C" {
 
 int skrp_synth_uniform_coords(int32_t *out, int64_t n, int64_t size, uint64_t seed, int32_t stream_id,
-                              skrp_stream_t stream)
+                              int64_t offset, skrp_stream_t stream)
 {
-    SKRP_REQUIRE(n >= 0 && size >= 1 && size < (int64_t(1) << 31), "uniform coords: bad size");
+    SKRP_REQUIRE(n >= 0 && offset >= 0 && size >= 1 && size < (int64_t(1) << 31), "uniform coords: bad size");
     if (n == 0) return SKRP_OK;
     SKRP_REQUIRE(out, "uniform coords: null output");
-    uniform_coords_kernel<<<grid_of((n + 3) / 4), 256, 0, (cudaStream_t)stream>>>(out, n, (uint64_t)size,
-                                                                                    seed, (uint32_t)stream_id);
+    uniform_coords_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(out, n, (uint64_t)size, seed,
+                                                                         (uint32_t)stream_id, offset);
     SKRP_LAUNCHED("uniform_coords_kernel");
     return SKRP_OK;
 }
 
 int skrp_synth_zipf_coords(int32_t *out, int64_t n, const double *cdf, int64_t size, uint64_t seed,
-                           int32_t stream_id, skrp_stream_t stream)
+                           int32_t stream_id, int64_t offset, skrp_stream_t stream)
 {
-    SKRP_REQUIRE(n >= 0 && size >= 1 && size < (int64_t(1) << 31), "zipf coords: bad size");
+    SKRP_REQUIRE(n >= 0 && offset >= 0 && size >= 1 && size < (int64_t(1) << 31), "zipf coords: bad size");
     if (n == 0) return SKRP_OK;
     SKRP_REQUIRE(out && cdf, "zipf coords: null pointer");
-    zipf_coords_kernel<<<grid_of((n + 1) / 2), 256, 0, (cudaStream_t)stream>>>(out, n, cdf, size, seed,
-                                                                                 (uint32_t)stream_id);
+    zipf_coords_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(out, n, cdf, size, seed,
+                                                                      (uint32_t)stream_id, offset);
     SKRP_LAUNCHED("zipf_coords_kernel");
     return SKRP_OK;
 }
@@ -127,3 +120,91 @@ int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed, skrp
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ dedup (K7)
+// First-occurrence de-duplication of coordinate tuples (synth.py:68-84 keeps
+// the first draw of every tuple).  Open-addressing hash table of element
+// indices: insert claims an empty slot with CAS, or -- when the slot holds an
+// equal tuple -- lowers it to the smaller index with atomicMin, so every
+// tuple's slot ends holding its first occurrence; an element is kept iff its
+// tuple's slot holds its own index.
+namespace skrp {
+struct TupleArgs {
+    const int32_t *coords[SKRP_MAX_MODES];
+};
+
+__device__ __forceinline__ uint64_t tuple_hash(const TupleArgs &a, int nm, int64_t i)
+{
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (int w = 0; w < nm; ++w) {
+        h ^= (uint64_t)(uint32_t)a.coords[w][i] + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+    }
+    return h;
+}
+
+__device__ __forceinline__ bool tuple_eq(const TupleArgs &a, int nm, int64_t i, int64_t j)
+{
+    for (int w = 0; w < nm; ++w)
+        if (a.coords[w][i] != a.coords[w][j]) return false;
+    return true;
+}
+
+constexpr unsigned long long kEmpty = 0xFFFFFFFFFFFFFFFFull;
+
+__global__ void dedup_insert_kernel(TupleArgs a, int nm, int64_t n, unsigned long long *table, uint64_t mask)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t slot = tuple_hash(a, nm, i) & mask;
+        for (;;) {
+            unsigned long long cur = table[slot];
+            if (cur == kEmpty) {
+                cur = atomicCAS(&table[slot], kEmpty, (unsigned long long)i);
+                if (cur == kEmpty) break;
+            }
+            if (tuple_eq(a, nm, (int64_t)cur, i)) {
+                atomicMin(&table[slot], (unsigned long long)i);
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+    }
+}
+
+__global__ void dedup_mark_kernel(TupleArgs a, int nm, int64_t n, const unsigned long long *table, uint64_t mask,
+                                  uint8_t *keep)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t slot = tuple_hash(a, nm, i) & mask;
+        for (;;) {
+            unsigned long long cur = table[slot];
+            if (tuple_eq(a, nm, (int64_t)cur, i)) {
+                keep[i] = (cur == (unsigned long long)i) ? 1 : 0;
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+    }
+}
+}  // namespace skrp
+
+extern "C" int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int64_t n, void *table,
+                               int64_t table_slots, uint8_t *keep, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(nmodes >= 1 && nmodes <= SKRP_MAX_MODES && n >= 0, "skrp_dedup_mark: bad sizes");
+    SKRP_REQUIRE(table_slots >= 2 * n && (table_slots & (table_slots - 1)) == 0,
+                 "skrp_dedup_mark: table_slots must be a power of two >= 2n");
+    if (n == 0) return SKRP_OK;
+    SKRP_REQUIRE(coords && table && keep, "skrp_dedup_mark: null pointer");
+    TupleArgs a{};
+    for (int w = 0; w < nmodes; ++w) a.coords[w] = coords[w];
+    cudaStream_t s = (cudaStream_t)stream;
+    SKRP_CUDA(cudaMemsetAsync(table, 0xFF, sizeof(unsigned long long) * table_slots, s));
+    uint64_t mask = (uint64_t)table_slots - 1;
+    dedup_insert_kernel<<<grid_of(n), 256, 0, s>>>(a, nmodes, n, (unsigned long long *)table, mask);
+    SKRP_LAUNCHED("dedup_insert_kernel");
+    dedup_mark_kernel<<<grid_of(n), 256, 0, s>>>(a, nmodes, n, (const unsigned long long *)table, mask, keep);
+    SKRP_LAUNCHED("dedup_mark_kernel");
+    return SKRP_OK;
+}

@@ -111,18 +111,8 @@ class DistributedMttkrp:
         if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
             self.prepare(rank_r, factors[0].dtype)
         facs = list(factors)
-        stream = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
         for d, plan in enumerate(self.plans):
-            out = self.outputs[d]
-            for lo, hi in self.ownership[d][self.rank]:
-                out[lo:hi].zero_()
-            if self.compute is not None:
-                self.compute(plan, self.mine[d], facs, out)
-            else:
-                coords, vals = _plan_arrays(plan, self.device)
-                ev = kernel_events[d] if kernel_events is not None else None
-                self._exec(d, rank_r).run(coords, vals, plan.nnz, plan.mode, facs, out, self.cfg,
-                                          stream.cuda_stream, events=ev)
+            out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d])
             if self.world > 1:
                 allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
             if after_mode is not None:
@@ -130,6 +120,27 @@ class DistributedMttkrp:
             if chained:
                 facs[plan.mode] = out
         return self.outputs
+
+    def mode_output(self, d, factors, events=None):
+        """Mode d's MTTKRP on this rank's shards into self.outputs[d]: owned
+        rows valid, nothing exchanged yet."""
+        import torch
+
+        rank_r = factors[0].shape[1]
+        if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
+            self.prepare(rank_r, factors[0].dtype)
+        plan = self.plans[d]
+        out = self.outputs[d]
+        for lo, hi in self.ownership[d][self.rank]:
+            out[lo:hi].zero_()
+        if self.compute is not None:
+            self.compute(plan, self.mine[d], factors, out)
+        else:
+            coords, vals = _plan_arrays(plan, self.device)
+            stream = torch.cuda.current_stream(self.device)
+            self._exec(d, rank_r).run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg,
+                                      stream.cuda_stream, events=events)
+        return out
 
     def needed_factors(self, chained=True):
         """Modes whose INPUT factor is actually read: with chaining, factor w
@@ -189,6 +200,152 @@ class DistributedMttkrp:
         comp.wait_stream(s_out)
         d2h = sum(moved)
         return h2d, d2h
+
+
+class DistributedCpAls:
+    """CP-ALS with one process per GPU (cpd.py:108-167 semantics; cfg5).
+
+    Per mode d, on every rank: MTTKRP of its own shards (owned output rows
+    only), V = Hadamard of the other modes' Grams (R x R, identical on all
+    ranks), W = V^-1 with the reference's jitter/pinv fallback (host, fp64),
+    new rows = M[owned] @ W (GPU), column norms = sqrt(all-reduce of per-rank
+    column sums of squares) -> lambdas, owned rows normalised, then the
+    FACTOR ALL-GATHER of the owned rows (every rank holds the full updated
+    factor) and Gram_d = all-reduce of the per-rank partial Grams.  The fit
+    sums <X, Xhat> and ||X||^2 over each rank's share of the nonzeros (the
+    mode-0 plan's owned shards partition them) and all-reduces the pair.
+    """
+
+    def __init__(self, plans, cfg: PlatformConfig, rank=None, world=None, group=None, device=None):
+        self.mt = DistributedMttkrp(plans, cfg, rank=rank, world=world, group=group, device=device)
+        self.group = group
+
+    def _allreduce(self, t):
+        if self.mt.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def _owned(self, d):
+        return self.mt.ownership[d][self.mt.rank]
+
+    def _partial_gram(self, y, d):
+        import torch
+
+        from . import _lib
+
+        R = y.shape[1]
+        g = torch.zeros((R, R), dtype=torch.float64, device=y.device)
+        tmp = torch.empty((R, R), dtype=torch.float64, device=y.device)
+        stream = torch.cuda.current_stream(y.device).cuda_stream
+        for lo, hi in self._owned(d):
+            if hi > lo:
+                _lib.call("skrp_gram", y[lo:hi].data_ptr(), hi - lo, R, tmp.data_ptr(), stream)
+                g += tmp
+        return self._allreduce(g).cpu().numpy()
+
+    def _col_sumsq(self, x, d):
+        import torch
+
+        from . import _lib
+
+        R = x.shape[1]
+        acc = torch.zeros(R, dtype=torch.float64, device=x.device)
+        tmp = torch.empty(R, dtype=torch.float64, device=x.device)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        for lo, hi in self._owned(d):
+            if hi > lo:
+                _lib.call("skrp_col_sumsq", x[lo:hi].data_ptr(), hi - lo, R, tmp.data_ptr(), stream)
+                acc += tmp
+        return self._allreduce(acc).cpu().numpy()
+
+    def _x_sq(self):
+        """||X||^2 over this rank's nonzeros (mode-0 plan's owned shards), summed."""
+        import torch
+
+        from . import _lib
+
+        if getattr(self, "_xsq", None) is None:
+            plan = self.mt.plans[0]
+            _, vals = _plan_arrays(plan, self.mt.device)
+            total = torch.zeros(1, dtype=torch.float64, device=self.mt.device)
+            out = torch.empty(1, dtype=torch.float64, device=self.mt.device)
+            stream = torch.cuda.current_stream(self.mt.device).cuda_stream
+            for j in self.mt.mine[0]:
+                sh = plan.shards[j]
+                if sh.nnz:
+                    _lib.call("skrp_sumsq", vals.data_ptr() + 4 * sh.start, sh.nnz, out.data_ptr(), stream)
+                    total += out
+            self._xsq = float(self._allreduce(total).item())
+        return self._xsq
+
+    def _inner_fused(self, d, new, m, lambdas):
+        """<X, Xhat> = sum_r lambda_r sum_i F_d[i, r] M_d[i, r] over owned rows of
+        the LAST mode d (M_d computed with the already-updated other factors):
+        the fit without a second pass over the nonzeros."""
+        import torch
+
+        from . import _lib
+
+        R = new.shape[1]
+        lam = torch.from_numpy(np.ascontiguousarray(lambdas, dtype=np.float64)).to(new.device)
+        total = torch.zeros(1, dtype=torch.float64, device=new.device)
+        out = torch.empty(1, dtype=torch.float64, device=new.device)
+        stream = torch.cuda.current_stream(new.device).cuda_stream
+        for lo, hi in self._owned(d):
+            if hi > lo:
+                _lib.call("skrp_weighted_dot", new[lo:hi].data_ptr(), m[lo:hi].data_ptr(), hi - lo, R,
+                          lam.data_ptr(), out.data_ptr(), stream)
+                total += out
+        return float(self._allreduce(total).item())
+
+    def run(self, factors, iterations=1, fit_tol=None, timings=None):
+        """ALS sweeps from the given full fp32 factor replicas (device).
+        Returns (factors, lambdas, fit_history)."""
+        import torch
+
+        from . import _lib
+        from .cpd import _fit_value, _hadamard, _solve_matrix
+
+        facs = [f.clone() for f in factors]
+        nm = len(facs)
+        R = facs[0].shape[1]
+        grams = [self._partial_gram(f, w) for w, f in enumerate(facs)]
+        lambdas = np.ones(R)
+        history = []
+        stream = torch.cuda.current_stream(self.mt.device).cuda_stream
+        for _ in range(iterations):
+            for d in range(nm):
+                m = self.mt.mode_output(d, facs)
+                if not np.isfinite(self._col_sumsq(m, d)).all():
+                    raise FloatingPointError("non-finite MTTKRP output")
+                v = _hadamard([grams[w] for w in range(nm) if w != d], R)
+                if not np.isfinite(v).all():
+                    raise FloatingPointError("non-finite Gram product")
+                w_t = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device)
+                new = torch.empty_like(m)
+                for lo, hi in self._owned(d):
+                    if hi > lo:
+                        _lib.call("skrp_apply_rr", m[lo:hi].data_ptr(), hi - lo, R, w_t.data_ptr(),
+                                  new[lo:hi].data_ptr(), stream)
+                lambdas = np.sqrt(self._col_sumsq(new, d))
+                if not np.isfinite(lambdas).all():
+                    raise FloatingPointError("non-finite entries in updated factor matrix")
+                scale = torch.from_numpy(1.0 / np.where(lambdas > 0, lambdas, 1.0)).to(m.device)
+                for lo, hi in self._owned(d):
+                    if hi > lo:
+                        _lib.call("skrp_scale_cols", new[lo:hi].data_ptr(), hi - lo, R, scale.data_ptr(), stream)
+                if d == nm - 1:
+                    inner = self._inner_fused(d, new, m, lambdas)
+                if self.mt.world > 1:
+                    allgather_owned_rows(new, self.mt.ownership[d], self.group)
+                facs[d] = new
+                grams[d] = self._partial_gram(new, d)
+            history.append(_fit_value(self._x_sq(), inner, grams, lambdas))
+            if fit_tol is not None and len(history) > 1 and history[-1] - history[-2] < fit_tol:
+                break
+        return facs, lambdas, history
 
 
 def ownership_table(plan, world: int, scheduling: str = "dynamic"):

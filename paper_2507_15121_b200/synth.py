@@ -98,35 +98,83 @@ def synth_tensor(shape, nnz, distribution="uniform", zipf_exponent=1.2, value_di
 
 
 def synth_tensor_device(shape, nnz, distribution="uniform", zipf_exponent=1.2,
-                        value_dist="uniform", seed=0, name="", device=None):
-    """Billion-scale generator on the GPU (Philox, same laws); see module doc.
+                        value_dist="uniform", seed=0, name="", device=None, unique=True):
+    """Billion-scale generator on the GPU (Philox, the reference's laws).
 
-    Coordinates are drawn independently per nonzero; duplicates are NOT
-    removed here (expected count for uniform draws is nnz^2 / (2 * prod(shape)),
-    0.09 for the Amazon-shaped config).  Returns a device-resident tensor.
+    Coordinates of draw g are a pure function of (seed, mode, g).  With
+    ``unique`` (default, like the reference) duplicate tuples are removed
+    keeping first occurrences and the pool is topped up with further draws
+    until `nnz` unique tuples exist -- the reference's rounds (synth.py:68-84:
+    batch = short + short//4 + 16, first occurrences kept, <= 200 rounds) run
+    on the GPU with a hash-table first-occurrence filter (skrp_dedup_mark).
+    Values are drawn after the coordinates, one per kept nonzero.
     """
     import torch
 
     from . import _lib
 
     shape = tuple(int(s) for s in shape)
+    nnz = int(nnz)
     if distribution not in ("uniform", "zipf"):
         raise ValueError(f"unknown distribution {distribution!r}")
     if value_dist not in ("uniform", "normal"):
         raise ValueError(f"unknown value_dist {value_dist!r}")
+    capacity = 1
+    for s_ in shape:
+        capacity *= s_
+    if nnz > capacity:
+        raise ValueError(f"nnz={nnz} infeasible for shape {shape} (capacity {capacity})")
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    coords = [torch.empty(nnz, dtype=torch.int32, device=dev) for _ in shape]
-    vals = torch.empty(nnz, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    for w, s in enumerate(shape):
-        if distribution == "uniform":
-            _lib.call("skrp_synth_uniform_coords", _lib.ptr(coords[w]), nnz, s, seed, w, stream)
-        else:
-            cdf = torch.from_numpy(zipf_cdf(s, zipf_exponent)).to(dev)
-            _lib.call("skrp_synth_zipf_coords", _lib.ptr(coords[w]), nnz, _lib.ptr(cdf), s, seed, w,
-                      stream)
-    _lib.call("skrp_synth_values", _lib.ptr(vals), nnz, 1 if value_dist == "normal" else 0, seed,
-              stream)
+    cdfs = ([torch.from_numpy(zipf_cdf(s_, zipf_exponent)).to(dev) for s_ in shape]
+            if distribution == "zipf" else None)
+
+    def draw(count, offset):
+        cols = [torch.empty(count, dtype=torch.int32, device=dev) for _ in shape]
+        for w, s_ in enumerate(shape):
+            if cdfs is None:
+                _lib.call("skrp_synth_uniform_coords", _lib.ptr(cols[w]), count, s_, seed, w, offset, stream)
+            else:
+                _lib.call("skrp_synth_zipf_coords", _lib.ptr(cols[w]), count, _lib.ptr(cdfs[w]), s_, seed, w,
+                          offset, stream)
+        return cols
+
+    dups = 0
+    if not unique:
+        coords = draw(nnz, 0)
+    else:
+        coords = [torch.empty(0, dtype=torch.int32, device=dev) for _ in shape]
+        drawn = 0
+        rounds = 0
+        while coords[0].numel() < nnz:
+            if rounds >= _MAX_ROUNDS - 1:
+                raise ValueError(
+                    f"could not collect {nnz} unique coordinates in {_MAX_ROUNDS} rounds; "
+                    "distribution too concentrated for requested nnz")
+            rounds += 1
+            short = nnz - coords[0].numel()
+            count = max(short + short // 4 + 16, 64)
+            batch = draw(count, drawn)
+            drawn += count
+            pool = [torch.cat([c, b]) for c, b in zip(coords, batch)]
+            del batch
+            n = pool[0].numel()
+            slots = 1
+            while slots < 2 * n:
+                slots *= 2
+            table = torch.empty(slots, dtype=torch.int64, device=dev)
+            keep = torch.empty(n, dtype=torch.uint8, device=dev)
+            cptr = (_lib.vp * len(pool))(*[c.data_ptr() for c in pool])
+            _lib.call("skrp_dedup_mark", cptr, len(pool), n, table.data_ptr(), slots, keep.data_ptr(), stream)
+            del table
+            mask = keep.bool()
+            kept = int(mask.sum().item())
+            dups += n - kept
+            coords = [c[mask] for c in pool]  # stable compaction: first occurrences, draw order
+            del pool, mask, keep
+        coords = [c[:nnz].contiguous() for c in coords]
+    vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("skrp_synth_values", _lib.ptr(vals), nnz, 1 if value_dist == "normal" else 0, seed, stream)
     return SparseTensorCOO.from_device(shape, coords, vals,
                                        name=name or f"synth-{distribution}-{seed}-device",
-                                       stats=LoadStats(nnz=nnz))
+                                       stats=LoadStats(nnz=nnz, duplicates=dups))

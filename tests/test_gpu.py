@@ -338,16 +338,16 @@ def test_cp_als_matches_reference_history(golden):
 
 
 def test_device_generator_laws():
-    t = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3)
+    t = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3, unique=False)
     idx = t.indices
     assert idx.max(axis=0).tolist() == [999, 99, 99] and idx.min() == 0
     assert abs(t.values.mean() - 0.5) < 2e-3 and t.values.min() >= 0 and t.values.max() < 1
-    z = sk.synth_tensor_device((1000, 100, 100), 1_000_000, distribution="zipf", seed=3)
+    z = sk.synth_tensor_device((1000, 100, 100), 1_000_000, distribution="zipf", seed=3, unique=False)
     cdf = sk.synth.zipf_cdf(1000, 1.2)
     head = np.mean(z.indices[:, 0] == 0)
     assert abs(head - cdf[0]) < 3e-3
     # same seed -> same tensor; other seed -> different
-    t2 = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3)
+    t2 = sk.synth_tensor_device((1000, 100, 100), 2_000_000, seed=3, unique=False)
     assert np.array_equal(t2.indices, idx)
 
 
@@ -435,3 +435,68 @@ def test_blocked_layout_through_runner(golden):
         expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
         assert rel_err(outs[d], expect) <= TOL
         facs[d] = outs[d]
+
+
+# ------------------------------------------------------------------- dedup
+
+
+def test_dedup_mark_first_occurrence():
+    rng = np.random.default_rng(3)
+    n = 200_000
+    idx = np.stack([rng.integers(0, s, n) for s in (20, 30, 7, 5)], 1)  # many duplicates
+    cols = [torch.from_numpy(idx[:, w].astype(np.int32)).cuda() for w in range(4)]
+    slots = 1 << 19
+    table = torch.empty(slots, dtype=torch.int64, device="cuda")
+    keep = torch.empty(n, dtype=torch.uint8, device="cuda")
+    import ctypes
+    cptr = (ctypes.c_void_p * 4)(*[c.data_ptr() for c in cols])
+    _lib.call("skrp_dedup_mark", cptr, 4, n, table.data_ptr(), slots, keep.data_ptr(), stream())
+    _, first = np.unique(idx, axis=0, return_index=True)
+    expect = np.zeros(n, dtype=np.uint8)
+    expect[first] = 1
+    assert np.array_equal(keep.cpu().numpy(), expect)
+
+
+def test_device_generator_unique_zipf():
+    t = sk.synth_tensor_device((60, 50, 40), 30_000, distribution="zipf", seed=4)
+    idx = t.indices
+    assert len(idx) == 30_000 and len(np.unique(idx, axis=0)) == 30_000
+    assert t.stats.duplicates > 0
+    # deterministic in the seed
+    t2 = sk.synth_tensor_device((60, 50, 40), 30_000, distribution="zipf", seed=4)
+    assert np.array_equal(t2.indices, idx)
+
+
+# ------------------------------------------------------- distributed CP-ALS
+
+
+def test_distributed_cp_als_world1_matches_reference(golden):
+    """DistributedCpAls (the cfg5 path) at world == 1 reproduces the
+    reference cp_als fit history and lambdas (same init, same updates)."""
+    from paper_2507_15121_b200.distributed import DistributedCpAls
+
+    t = sk.synth_tensor((30, 20, 10), 1500, seed=9)
+    ref = golden("cpd.npz")
+    plans = sk.build_all_plans(t, sk.PartitionConfig())
+    als = DistributedCpAls(plans, sk.PlatformConfig(rank=4))
+    init = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in sk.random_factors(t.shape, 4, seed=1)]
+    facs, lam, hist = als.run(init, iterations=3)
+    assert np.allclose(hist, ref["u_engine_fit"], rtol=0, atol=2e-4)
+    assert np.allclose(lam, ref["u_engine_lambdas"], rtol=2e-3)
+    for w, f in enumerate(facs):
+        assert np.allclose(f.double().cpu().numpy(), ref[f"u_engine_F{w}"], atol=2e-3)
+
+
+def test_distributed_cp_als_rank4_blocked_atomic(golden):
+    from paper_2507_15121_b200.distributed import DistributedCpAls
+
+    rng = np.random.default_rng(5)
+    a, b, c = (rng.random((n, 4)) for n in (40, 30, 20))
+    dense = np.einsum("ir,jr,kr->ijk", a, b, c)
+    idx = np.argwhere(np.ones_like(dense, dtype=bool))
+    t = sk.SparseTensorCOO(dense.shape, idx, dense[tuple(idx.T)])
+    plans = sk.build_all_plans(t, sk.PartitionConfig(strategy="nnz-balanced"))
+    als = DistributedCpAls(plans, sk.PlatformConfig(rank=4, accumulation="atomic"))
+    init = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in sk.random_factors(t.shape, 4, seed=0)]
+    _, _, hist = als.run(init, iterations=25)
+    assert hist[-1] > 0.99 and abs(hist[-1] - golden("cpd.npz")["r4_fit"][-1]) < 1e-3

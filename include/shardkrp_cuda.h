@@ -85,6 +85,12 @@ int skrp_block_keys(const uint32_t *const *coords, int32_t nmodes, const int32_t
                     const int32_t *widths, const int64_t *shard_starts, int64_t nshards,
                     int32_t shard_bits, int64_t nnz, uint32_t *keys, skrp_stream_t stream);
 
+/* Distributed plan build: dest[i] = owner[j] for the shard j
+ * with bounds[j] <= keys[i] < bounds[j+1] (bounds: k+1 device int64, owner: k
+ * device int32) -- the routing step of the per-rank bucket exchange. */
+int skrp_route_by_bounds(const uint32_t *keys, int64_t n, const int64_t *bounds, int64_t k,
+                         const int32_t *owner, uint32_t *dest, skrp_stream_t stream);
+
 /* ------------------------------------------------------------ MTTKRP (K1) */
 typedef struct {
     int32_t nmodes;                          /* N, 3..SKRP_MAX_MODES                */
@@ -135,7 +141,7 @@ int skrp_synth_uniform_coords(int32_t *out, int64_t n, int64_t size, uint64_t se
                               int32_t stream_id, int64_t offset, skrp_stream_t stream);
 int skrp_synth_zipf_coords(int32_t *out, int64_t n, const double *cdf, int64_t size,
                            uint64_t seed, int32_t stream_id, int64_t offset, skrp_stream_t stream);
-int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed,
+int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed, int64_t offset,
                       skrp_stream_t stream);
 /* keep[i] = 1 iff element i is the first occurrence of its coordinate tuple
  * (synth.py:68-84 dedup rule).  table: caller scratch of table_slots uint64

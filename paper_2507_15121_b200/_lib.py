@@ -70,7 +70,8 @@ SIGNATURES = {
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),
     "skrp_synth_uniform_coords": (i32, [vp, i64, i64, u64, i32, i64, vp]),
     "skrp_synth_zipf_coords": (i32, [vp, i64, vp, i64, u64, i32, i64, vp]),
-    "skrp_synth_values": (i32, [vp, i64, i32, u64, vp]),
+    "skrp_synth_values": (i32, [vp, i64, i32, u64, i64, vp]),
+    "skrp_route_by_bounds": (i32, [vp, i64, vp, i64, vp, vp, vp]),
     "skrp_dedup_mark": (i32, [vp, i32, i64, vp, i64, vp, vp]),
     "skrp_gram": (i32, [vp, i64, i32, vp, vp]),
     "skrp_apply_rr": (i32, [vp, i64, i32, vp, vp, vp]),

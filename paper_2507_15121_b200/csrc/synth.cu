@@ -52,23 +52,19 @@ __global__ void zipf_coords_kernel(int32_t *out, int64_t n, const double *__rest
     }
 }
 
-__global__ void values_kernel(float *out, int64_t n, int normal, uint64_t seed)
+__global__ void values_kernel(float *out, int64_t n, int normal, uint64_t seed, int64_t offset)
 {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t pairs = (n + 1) / 2;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < pairs; q += stride) {
-        Philox4 r = philox4x32_10((uint32_t)q, (uint32_t)(q >> 32), 0xFFFFu, 0x5EED0003u, (uint32_t)seed,
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t g = (uint64_t)(offset + i);
+        Philox4 r = philox4x32_10((uint32_t)g, (uint32_t)(g >> 32), 0xFFFFu, 0x5EED0003u, (uint32_t)seed,
                                   (uint32_t)(seed >> 32));
-        double a = u53(r.x, r.y), b = u53(r.z, r.w);
-        double v0 = a, v1 = b;
+        double v = u53(r.x, r.y);
         if (normal) {  // Box-Muller
-            double rad = sqrt(-2.0 * log(1.0 - a));
-            v0 = rad * cos(2.0 * M_PI * b);
-            v1 = rad * sin(2.0 * M_PI * b);
+            const double b = u53(r.z, r.w);
+            v = sqrt(-2.0 * log(1.0 - v)) * cos(2.0 * M_PI * b);
         }
-        int64_t i = 2 * q;
-        out[i] = (float)v0;
-        if (i + 1 < n) out[i + 1] = (float)v1;
+        out[i] = (float)v;
     }
 }
 
@@ -109,12 +105,12 @@ int skrp_synth_zipf_coords(int32_t *out, int64_t n, const double *cdf, int64_t s
     return SKRP_OK;
 }
 
-int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed, skrp_stream_t stream)
+int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed, int64_t offset, skrp_stream_t stream)
 {
-    SKRP_REQUIRE(n >= 0, "values: negative n");
+    SKRP_REQUIRE(n >= 0 && offset >= 0, "values: negative n/offset");
     if (n == 0) return SKRP_OK;
     SKRP_REQUIRE(out, "values: null output");
-    values_kernel<<<grid_of((n + 1) / 2), 256, 0, (cudaStream_t)stream>>>(out, n, normal ? 1 : 0, seed);
+    values_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(out, n, normal ? 1 : 0, seed, offset);
     SKRP_LAUNCHED("values_kernel");
     return SKRP_OK;
 }
@@ -206,5 +202,34 @@ extern "C" int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int
     SKRP_LAUNCHED("dedup_insert_kernel");
     dedup_mark_kernel<<<grid_of(n), 256, 0, s>>>(a, nmodes, n, (const unsigned long long *)table, mask, keep);
     SKRP_LAUNCHED("dedup_mark_kernel");
+    return SKRP_OK;
+}
+
+// -------------------------------------------------- distributed plan build
+// dest[i] = owner[shard(key[i])], shard(c) = last j with bounds[j] <= c
+namespace skrp {
+__global__ void route_kernel(const uint32_t *__restrict__ keys, int64_t n, const int64_t *__restrict__ bounds,
+                             int64_t k, const int32_t *__restrict__ owner, uint32_t *dest)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = keys[i];
+        int64_t lo = 0, hi = k;  // bounds[lo] <= c < bounds[hi]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (bounds[mid] <= c) lo = mid; else hi = mid;
+        }
+        dest[i] = (uint32_t)owner[lo];
+    }
+}
+}  // namespace skrp
+
+extern "C" int skrp_route_by_bounds(const uint32_t *keys, int64_t n, const int64_t *bounds, int64_t k,
+                                    const int32_t *owner, uint32_t *dest, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(n >= 0 && k >= 1, "skrp_route_by_bounds: bad sizes");
+    if (n == 0) return SKRP_OK;
+    SKRP_REQUIRE(keys && bounds && owner && dest, "skrp_route_by_bounds: null pointer");
+    route_kernel<<<grid_of(n), 256, 0, (cudaStream_t)stream>>>(keys, n, bounds, k, owner, dest);
+    SKRP_LAUNCHED("route_kernel");
     return SKRP_OK;
 }

@@ -51,7 +51,9 @@ class DistributedMttkrp:
         self.ownership = []
         self.mine = []
         for p in self.plans:
-            a = assign_shards(p, self.world, cfg.scheduling)
+            # plans built by distplan carry GLOBAL shard sizes (local ones are
+            # zero for shards other ranks own): place on those, like the build did
+            a = assign_shards(p, self.world, cfg.scheduling, weights=getattr(p, "global_shard_nnz", None))
             self.assignment.append(a)
             self.ownership.append([_normalize_ranges([p.shards[j].index_range for j in a[r]])
                                    for r in range(self.world)])

@@ -174,7 +174,39 @@ def synth_tensor_device(shape, nnz, distribution="uniform", zipf_exponent=1.2,
             del pool, mask, keep
         coords = [c[:nnz].contiguous() for c in coords]
     vals = torch.empty(nnz, dtype=torch.float32, device=dev)
-    _lib.call("skrp_synth_values", _lib.ptr(vals), nnz, 1 if value_dist == "normal" else 0, seed, stream)
+    _lib.call("skrp_synth_values", _lib.ptr(vals), nnz, 1 if value_dist == "normal" else 0, seed, 0, stream)
     return SparseTensorCOO.from_device(shape, coords, vals,
                                        name=name or f"synth-{distribution}-{seed}-device",
                                        stats=LoadStats(nnz=nnz, duplicates=dups))
+
+
+def synth_tensor_chunk(shape, nnz, rank, world, distribution="uniform", zipf_exponent=1.2,
+                       value_dist="uniform", seed=0, device=None):
+    """Rank `rank`'s contiguous chunk [nnz*rank//world, nnz*(rank+1)//world) of
+    the global draw stream (counter-based: identical to the single-GPU draws
+    of those elements), for the distributed plan build (distplan.py).  No
+    de-duplication across the chunk boundary is possible here; see DESIGN.md."""
+    import torch
+
+    from . import _lib
+
+    shape = tuple(int(s) for s in shape)
+    lo = nnz * rank // world
+    hi = nnz * (rank + 1) // world
+    n = hi - lo
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    coords = [torch.empty(n, dtype=torch.int32, device=dev) for _ in shape]
+    for w, s_ in enumerate(shape):
+        if distribution == "uniform":
+            _lib.call("skrp_synth_uniform_coords", _lib.ptr(coords[w]), n, s_, seed, w, lo, stream)
+        else:
+            cdf = torch.from_numpy(zipf_cdf(s_, zipf_exponent)).to(dev)
+            _lib.call("skrp_synth_zipf_coords", _lib.ptr(coords[w]), n, _lib.ptr(cdf), s_, seed, w, lo, stream)
+    vals = torch.empty(n, dtype=torch.float32, device=dev)
+    _lib.call("skrp_synth_values", _lib.ptr(vals), n, 1 if value_dist == "normal" else 0, seed, lo, stream)
+    t = SparseTensorCOO.from_device(shape, coords, vals, name=f"synth-{distribution}-{seed}-chunk{rank}of{world}",
+                                    stats=LoadStats(nnz=n))
+    t.global_offset = lo
+    t.global_nnz = nnz
+    return t

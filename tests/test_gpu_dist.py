@@ -1,0 +1,113 @@
+"""Multi-process paths on one GPU: 2 ranks (gloo, both on cuda:0).
+
+Covers the one-process-per-GPU code the 8-GPU runs use -- distributed plan
+build (histogram all-reduce, bounds, placement, routed all-to-all, local
+stable sort) and DistributedMttkrp / DistributedCpAls with the owned-row
+all-gather -- against the single-process plan and the CPU oracle.  NCCL
+itself needs one GPU per rank, so the collectives run under gloo here.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_2507_15121_b200 as sk
+        from paper_2507_15121_b200.distplan import build_mode_plan_distributed
+        from paper_2507_15121_b200.distributed import DistributedCpAls, DistributedMttkrp
+        from paper_2507_15121_b200.synth import synth_tensor_chunk, synth_tensor_device
+
+        for shape, nnz, dist_law, strategy in [((300, 200, 100), 400_000, "uniform", "equal-index"),
+                                               ((500, 80, 60, 7), 300_000, "zipf", "nnz-balanced")]:
+            # the chunk generator reproduces its slice of the global draw stream
+            raw = synth_tensor_device(shape, nnz, distribution=dist_law, seed=6, unique=False)
+            ch = synth_tensor_chunk(shape, nnz, rank, world, distribution=dist_law, seed=6)
+            lo, hi = nnz * rank // world, nnz * (rank + 1) // world
+            rc, rv = raw.device_arrays()
+            cc, cv = ch.device_arrays()
+            assert all(torch.equal(a[lo:hi], b) for a, b in zip(rc, cc)) and torch.equal(rv[lo:hi], cv)
+            # plans are built from contiguous slices of a de-duplicated tensor
+            full = synth_tensor_device(shape, nnz, distribution=dist_law, seed=6)
+            fc, fv = full.device_arrays()
+            chunk = sk.SparseTensorCOO.from_device(shape, [c[lo:hi].contiguous() for c in fc], fv[lo:hi].contiguous())
+            pcfg = sk.PartitionConfig(devices=world, strategy=strategy, isp_capacity=1000)
+            ref_plans = sk.build_all_plans(full, pcfg)
+            plans = [build_mode_plan_distributed(chunk, d, pcfg) for d in range(len(shape))]
+            for rp, lp in zip(ref_plans, plans):
+                assert np.array_equal(lp.bounds, rp.bounds)
+                assert np.array_equal(lp.global_shard_nnz, [s.nnz for s in rp.shards])
+                owned = [j for j in range(rp.shard_count) if lp.shard_owner[j] == rank]
+                for j in owned:
+                    a, b = rp.shards[j].start, rp.shards[j].stop
+                    la, lb = lp.shards[j].start, lp.shards[j].stop
+                    assert lb - la == b - a
+                    for w in range(len(shape)):
+                        assert torch.equal(lp.coords[w][la:lb], rp.coords[w][a:b])
+                    assert torch.equal(lp.vals[la:lb], rp.vals[a:b])
+            fs = sk.random_factors(shape, 16, seed=1)
+            dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+            for acc, layout in [("deterministic-reduce", "flycoo"), ("atomic", "blocked")]:
+                cfg = sk.PlatformConfig(devices=world, rank=16, accumulation=acc, layout=layout, l2_budget_mb=0,
+                                        tile_nnz=64)
+                lplans = [build_mode_plan_distributed(chunk, d, pcfg) for d in range(len(shape))]
+                runner = DistributedMttkrp(lplans, cfg)
+                outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+                facs = [f.data.copy() for f in fs]
+                for d in range(len(shape)):
+                    expect = oracle.mttkrp_seq_c(full.indices, full.values, facs, d)
+                    err = np.max(np.abs(outs[d] - expect) / np.maximum(np.abs(expect), 1.0))
+                    assert err <= 1e-4, (d, acc, err)
+                    facs[d] = outs[d]
+            # CP-ALS across the two ranks == single process
+            als = DistributedCpAls(plans, sk.PlatformConfig(devices=world, rank=16))
+            _, lam2, h2 = als.run(dev_f, iterations=2)
+            single = DistributedCpAls(ref_plans, sk.PlatformConfig(devices=1, rank=16), rank=0, world=1)
+            _, lam1, h1 = single.run(dev_f, iterations=2)
+            assert np.allclose(h1, h2, atol=1e-4), (h1, h2)
+            assert np.allclose(lam1, lam2, rtol=1e-3), (np.max(np.abs(lam1 - lam2) / np.abs(lam1)), h1, h2)
+        q.put((rank, "ok"))
+    except Exception as exc:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()[-3000:]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_distributed_build_and_runs():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

@@ -59,6 +59,16 @@ CONFIGS = {
     "cfg4s": dict(shape=(8_200_000, 177_000, 8_100_000), nnz=500_000_000, rank=32, dist="zipf",
                   strategy="nnz-balanced", modes=None, host_gen=False,
                   desc="cfg4 Reddit-shaped 8.2Mx177Kx8.1M Zipf(1.2), R=32, all modes, 0.5B nnz (of 4.7B)"),
+    # full multi-GPU configs (distributed plan build; one GPU cannot hold them)
+    "cfg3": dict(shape=(46, 240_000, 240_000), nnz=3_600_000_000, rank=32, dist="uniform",
+                 strategy="equal-index", modes=None, host_gen=False, dist_build=True,
+                 desc="cfg3 Patents-shaped 46x240Kx240K, 3.6B nnz uniform, R=32, all modes"),
+    "cfg4": dict(shape=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, rank=32, dist="zipf",
+                 strategy="nnz-balanced", modes=None, host_gen=False, dist_build=True,
+                 desc="cfg4 Reddit-shaped 8.2Mx177Kx8.1M, 4.7B nnz Zipf(1.2), R=32, all modes"),
+    "cfg5": dict(shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=2_000_000_000, rank=64, dist="zipf",
+                 strategy="nnz-balanced", modes=None, host_gen=False, kind="cpd", dist_build=True,
+                 desc="cfg5 4-mode 10Mx1Mx100Kx1K, 2B nnz Zipf(1.2), R=64, one full CPD-ALS iteration"),
     "cfg5s": dict(shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=200_000_000, rank=64, dist="zipf",
                   strategy="nnz-balanced", modes=None, host_gen=False, kind="cpd",
                   desc="cfg5 4-mode 10Mx1Mx100Kx1K Zipf(1.2), R=64, one full CPD-ALS iteration, 0.2B nnz (of 2B)"),
@@ -257,11 +267,24 @@ def run_ours(args, cfg):
                            max_blocks=args.max_blocks)
 
     t_setup = time.perf_counter()
-    if cfg["host_gen"]:
+    dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
+    if world == 1 and cfg.get("dist_build", False):
+        raise SystemExit(f"{args.config} does not fit one B200 ({nnz} nnz); run it with torchrun --nproc-per-node >= 2 "
+                         f"or use the single-GPU '{args.config}s' variant")
+    if dist_build:
+        # each rank draws only its contiguous chunk of the global stream and
+        # receives its shards' nonzeros (distplan.py); no rank holds the tensor
+        from paper_2507_15121_b200.distplan import build_mode_plan_distributed
+        from paper_2507_15121_b200.synth import synth_tensor_chunk
+
+        tensor = synth_tensor_chunk(shape, nnz, rank, world, distribution=cfg["dist"], seed=0)
+        plans = [build_mode_plan_distributed(tensor, d, pcfg) for d in modes]
+    elif cfg["host_gen"]:
         tensor = sk.synth_tensor(shape, nnz, distribution=cfg["dist"], seed=0)
+        plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
     else:
         tensor = sk.synth_tensor_device(shape, nnz, distribution=cfg["dist"], seed=0)
-    plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
+        plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
     build_s = [p.build_time for p in plans]
     tensor.drop_device()
     torch.cuda.empty_cache()
@@ -363,7 +386,8 @@ def run_ours(args, cfg):
     # ---- parity on a seeded sample of output rows (chained replay, fp64)
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = sample_parity(plans, init, runner.outputs, modes, rows_per_mode=args.parity_rows)
+        parity = sample_parity(plans, init, runner.outputs, modes, rows_per_mode=args.parity_rows,
+                               owned=[runner.ownership[i][rank] for i in range(len(modes))] if dist_build else None)
 
     # ---- CPU baseline (rank 0, N=1 only): the C oracle port on a sample
     cpu = None
@@ -493,7 +517,7 @@ def cpu_mode0(shape, nnz, rank, threads):
     return nnz / best, best
 
 
-def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0, nnz_budget=8_000_000):
+def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0, nnz_budget=8_000_000, owned=None):
     """max |gpu - ref| / max(|ref|, 1) over a seeded sample of output rows
     per mode (rows added while their nonzeros fit `nnz_budget`; at least one
     row), ref recomputed in fp64 from the plan's nonzeros with the chained
@@ -509,9 +533,13 @@ def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0, nnz_bu
     rng = np.random.default_rng(seed)
     for i, (p, d) in enumerate(zip(plans, modes)):
         col = p.coords[d]
-        cand = rng.permutation(p.shape[d])[: 4 * rows_per_mode]
+        if owned is None:
+            pool_rows = np.arange(p.shape[d])
+        else:  # distributed build: only this rank's rows have their nonzeros here
+            pool_rows = np.concatenate([np.arange(lo, hi) for lo, hi in owned[i]] or [np.zeros(0, np.int64)])
+        cand = rng.permutation(pool_rows)[: 4 * rows_per_mode]
         member = torch.zeros(p.shape[d], dtype=torch.bool, device=dev)
-        member[torch.from_numpy(np.sort(cand[:rows_per_mode])).to(dev)] = True
+        member[torch.from_numpy(np.sort(cand[:rows_per_mode]).astype(np.int64)).to(dev)] = True
         # count nonzeros of the candidate rows, drop rows beyond the budget
         hits = torch.zeros(p.shape[d], dtype=torch.int64, device=dev)
         chunk = 1 << 27
@@ -520,6 +548,10 @@ def sample_parity(plans, init, outputs, modes, rows_per_mode=512, seed=0, nnz_bu
             m = member[c]
             hits.index_add_(0, c[m], torch.ones(int(m.sum().item()), dtype=torch.int64, device=dev))
         rows_all = np.sort(cand[:rows_per_mode])
+        if len(rows_all) == 0:
+            facs = list(facs)
+            facs[d] = outputs[i].double()
+            continue
         h = hits[torch.from_numpy(rows_all).to(dev)].cpu().numpy()
         keep, tot = [], 0
         for r, n in zip(rows_all, h):
@@ -572,6 +604,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
+    ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         print("note: warmup < 3 is below the timing rules; proceeding", file=sys.stderr)

@@ -340,7 +340,7 @@ static bool pick_v2(int R, Variant &v)
     switch (R) {
     case 8: v = mk2<NM, 1, 1, 3>(); return true;
     case 16: v = mk2<NM, 2, (NM == 3 ? 2 : 1), 3>(); return true;
-    case 32: v = mk2<NM, 4, 2, 3>(); return true;
+    case 32: v = (NM == 3) ? mk2<NM, 4, 4, 2>() : mk2<NM, 4, 2, 3>(); return true;
     case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2>(); return true;
     case 128: v = mk2<NM, 16, (NM == 3 ? 2 : 1), 2>(); return true;
     default: return false;
@@ -402,9 +402,13 @@ static Variant choose(const skrp_mttkrp_args &a)
             if (a.nmodes == 3) return mk2<3, 4, 2, 2>();
             if (a.nmodes == 4) return mk2<4, 4, 2, 2>();
         }
-        if (a.variant == 8 && a.rank == 32) {
-            if (a.nmodes == 3) return mk2<3, 4, 4, 2>();
+        if (a.variant == 8 && a.rank == 32) {  // previous default: U=2, 24 warps/SM
+            if (a.nmodes == 3) return mk2<3, 4, 2, 3>();
             if (a.nmodes == 4) return mk2<4, 4, 4, 2>();
+        }
+        if (a.variant == 9 && a.rank == 64) {
+            if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
+            if (a.nmodes == 4) return mk2<4, 8, 4, 1>();
         }
         if (a.variant == 0) {
             if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;

@@ -110,18 +110,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             if (shared && det && lane == 0) a.carry_rows[2 * t] = (int32_t)row;
         };
 
+        // batch metadata is software-pipelined: batch i+1's coordinates and
+        // values are requested before batch i's gathers, so the row test and
+        // the gather addresses never wait on a fresh metadata miss
+        uint32_t nr_l, nc_l[NIN];
+        float nv_l;
+        auto fetch = [&](int64_t nbase) {
+            const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
+            const bool v = lane < nn;
+            const int64_t src = nbase + (v ? lane : nn - 1);
+            nr_l = ld_stream_u32(rowc + src, pol_stream);
+            nv_l = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
+#pragma unroll
+            for (int j = 0; j < NIN; ++j) nc_l[j] = ld_stream_u32(C[j] + src, pol_stream);
+        };
+        fetch(b0);
         for (int64_t base = b0; base < b1; base += 32) {
             // a short last batch is padded with copies of its last nonzero
             // carrying value 0: same row (no extra boundary), valid
             // addresses, zero contribution -- so no per-element predicates
             const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
-            const bool lv = lane < nin;
-            const int64_t src = base + (lv ? lane : nin - 1);
-            const uint32_t r_l = ld_stream_u32(rowc + src, pol_stream);
-            const float v_l = lv ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
+            const uint32_t r_l = nr_l;
+            const float v_l = nv_l;
             uint32_t c_l[NIN];
 #pragma unroll
-            for (int j = 0; j < NIN; ++j) c_l[j] = ld_stream_u32(C[j] + src, pol_stream);
+            for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
+            if (base + 32 < b1) fetch(base + 32);
             const bool uniform = __all_sync(kFull, r_l == cur);
 
             // Batch classes: 0 = every row is `cur` (registers only);

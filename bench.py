@@ -263,6 +263,7 @@ def run_ours(args, cfg):
     modes = list(range(len(shape))) if cfg["modes"] is None else cfg["modes"]
     pcfg = sk.PartitionConfig(devices=world, strategy=cfg["strategy"])
     pl = sk.PlatformConfig(devices=world, rank=R, accumulation=args.accumulation, tile_nnz=args.tile,
+                           scheduling=args.scheduling,
                            kernel_variant=args.variant, layout=args.layout, l2_budget_mb=args.l2_mb,
                            max_blocks=args.max_blocks)
 
@@ -278,7 +279,7 @@ def run_ours(args, cfg):
         from paper_2507_15121_b200.synth import synth_tensor_chunk
 
         tensor = synth_tensor_chunk(shape, nnz, rank, world, distribution=cfg["dist"], seed=0)
-        plans = [build_mode_plan_distributed(tensor, d, pcfg) for d in modes]
+        plans = [build_mode_plan_distributed(tensor, d, pcfg, scheduling=args.scheduling) for d in modes]
     elif cfg["host_gen"]:
         tensor = sk.synth_tensor(shape, nnz, distribution=cfg["dist"], seed=0)
         plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
@@ -412,7 +413,7 @@ def run_ours(args, cfg):
                        "accumulation": args.accumulation, "tile_nnz": runner._exec(0, R).tile_nnz,
                        "layout": [p.layout for p in plans],
                        "block_shifts": [p.block_shifts for p in plans],
-                       "parallelism": f"output-row shards x{world}",
+                       "parallelism": f"output-row shards x{world}", "scheduling": args.scheduling,
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -605,6 +606,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
+    ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous"),
+                    help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         print("note: warmup < 3 is below the timing rules; proceeding", file=sys.stderr)

@@ -40,7 +40,10 @@ from .partition import ModePartitionPlan, PartitionConfig, TensorShard, build_mo
 from .tensor import FactorMatrix, NonzeroElement
 
 ACCUMULATION_MODES = ("deterministic-reduce", "atomic")
-SCHEDULING_MODES = ("dynamic", "static")
+# "contiguous" (B200 addition): each device gets one run of consecutive shards
+# cut at the cumulative-nnz targets, so its output rows form ONE range and the
+# inter-mode all-gather is one broadcast per device
+SCHEDULING_MODES = ("dynamic", "static", "contiguous")
 
 
 @dataclass(frozen=True)
@@ -149,7 +152,9 @@ def elementwise_compute(x: NonzeroElement, factors, mode: int):
 def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None) -> list:
     """Shard ids per device.
 
-    static  -- round-robin j::m (engine.py:291-293);
+    static     -- round-robin j::m (engine.py:291-293);
+    contiguous -- one run of consecutive shards per device, cut at the
+                  cumulative-cost targets (one owned row range per device);
     dynamic -- the reference's shared claim queue replayed deterministically:
                shards in order, each to the device that frees up first under
                cost = nnz (or ``weights``); ties to the lowest device id.
@@ -158,6 +163,19 @@ def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None
     if scheduling == "static":
         return [list(range(j, k, m)) for j in range(m)]
     cost = np.array([s.nnz for s in plan.shards] if weights is None else weights, dtype=np.float64)
+    if scheduling == "contiguous":
+        # cut the shard sequence at the prefix closest to j*total/m (every
+        # device gets at least one shard while shards remain)
+        pre = np.concatenate([[0.0], np.cumsum(cost)])
+        total = pre[-1]
+        cuts = [0]
+        for j in range(1, m):
+            lo = cuts[-1] + (1 if cuts[-1] < k - (m - j) else 0)
+            hi = max(lo, k - (m - j))
+            window = pre[lo:hi + 1]
+            cuts.append(lo + int(np.argmin(np.abs(window - j * total / m))) if len(window) else lo)
+        cuts.append(k)
+        return [list(range(cuts[j], cuts[j + 1])) for j in range(m)]
     load = np.zeros(m)
     out = [[] for _ in range(m)]
     for j in range(k):

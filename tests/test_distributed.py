@@ -67,7 +67,7 @@ def _worker(rank, world, port, q):
     try:
         s = np.load(os.path.join(os.path.dirname(__file__), "golden", "synth.npz"))
         for name, strategy, sched in [("z3", "nnz-balanced", "dynamic"), ("u5", "equal-index", "static"),
-                                      ("u3", "equal-index", "dynamic")]:
+                                      ("u3", "equal-index", "contiguous")]:
             idx, vals = s[f"{name}_indices"], s[f"{name}_values"]
             shape = tuple(int(x) for x in s[f"{name}_shape"])
             facs0 = [s[f"{name}_F8_{w}"] for w in range(len(shape))]

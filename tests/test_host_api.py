@@ -189,6 +189,20 @@ def test_assign_shards_static_and_dynamic():
     assert max(loads) - min(loads) <= 10
 
 
+@pytest.mark.parametrize("counts,m", [([10, 1, 1, 1, 10, 1], 2), ([5] * 32, 8), ([1] * 3, 8), ([100, 0, 0, 1], 3),
+                                      ([7, 9, 3, 8, 8, 1, 5, 2], 4)])
+def test_assign_shards_contiguous(counts, m):
+    plan = _FakePlan(counts, 4)
+    parts = sk.assign_shards(plan, m, "contiguous")
+    flat = sum(parts, [])
+    assert flat == list(range(len(counts)))  # consecutive runs, in order, covering all shards
+    assert all(p == list(range(p[0], p[-1] + 1)) for p in parts if p)
+    if len(counts) >= m:
+        assert all(len(p) >= 1 for p in parts)
+    loads = [sum(counts[j] for j in p) for p in parts]
+    assert max(loads) <= sum(counts) / m + max(counts)
+
+
 def test_ring_all_gather_host_buffers_match_reference_ledger(golden):
     for case in golden("ring.json"):
         m, rows = case["m"], case["rows"]

@@ -102,6 +102,14 @@ __device__ __forceinline__ void ld_row<4>(float (&v)[4], const float *p, uint64_
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
 }
 
+// no eviction hint (A/B of the L2 policy)
+__device__ __forceinline__ void ld_row8_plain(float (&v)[8], const float *p)
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
+
 template <>
 __device__ __forceinline__ void ld_row<1>(float (&v)[1], const float *p, uint64_t pol)
 {

@@ -325,11 +325,11 @@ static Variant mk()
     return v;
 }
 
-template <int NM, int LPN, int U, int MINB>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0>
 static Variant mk2()
 {
     Variant v;
-    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB>;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN>;
     v.smem = v2_smem_bytes<8 * LPN>();
     return v;
 }
@@ -406,6 +406,7 @@ static Variant choose(const skrp_mttkrp_args &a)
             if (a.nmodes == 3) return mk2<3, 4, 2, 3>();
             if (a.nmodes == 4) return mk2<4, 4, 4, 2>();
         }
+        if (a.variant == 10 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1>();  // no L2 hint
         if (a.variant == 9 && a.rank == 64) {
             if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
             if (a.nmodes == 4) return mk2<4, 8, 4, 1>();

@@ -21,7 +21,7 @@
 
 #include <type_traits>
 
-template <int NM, int LPN, int U, int MINB>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     mttkrp_v2_kernel(const skrp_mttkrp_args a, int additive)
 {
@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                        ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
+                        if constexpr (PLAIN) ld_row8_plain(g[u][j], F[j] + (size_t)idx * RR + col);
+                        else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
                     }
                 }
                 if (cls == 0) {

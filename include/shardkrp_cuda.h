@@ -54,7 +54,10 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* skrp_mttkrp_args.flags */
 #define SKRP_FLAG_ADDITIVE 1     /* rows may also get contributions from other tile
-                                    groups (blocked layouts): every flush adds   */
+                                    groups (blocked layouts): every flush adds --
+                                    red under SKRP_ACC_ATOMIC; under deterministic
+                                    accumulation the caller launches one block
+                                    group at a time and flushes read-add-write */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
@@ -121,11 +124,12 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);
  * chunks: 2*n_chunks [begin, end) entry ranges (never straddling a shard);
  * final_flags[c] != 0: every row of chunk c is complete -> written to out.
  * Otherwise the chunk's first/last row partials go to rows_out/vals_out at
- * entries 2c, 2c+1 (-1 rows when absent), in fp64. */
+ * entries 2c, 2c+1 (-1 rows when absent), in fp64.  additive != 0: completed
+ * rows are added to out (blocked layouts, one launch per block group). */
 int skrp_carry_fixup(const int32_t *rows_in, const void *vals_in, int32_t vals_in_is_f64,
                      const int64_t *chunks, const uint8_t *final_flags, int64_t n_chunks,
                      int32_t rank, float *out, int32_t *rows_out, double *vals_out,
-                     skrp_stream_t stream);
+                     int32_t additive, skrp_stream_t stream);
 
 /* Host-buffer convenience (allocates internally; not a hot call):
  * indices (nnz x N, uint64, row-major), values float64, factors[w] float64

@@ -66,7 +66,7 @@ SIGNATURES = {
     "skrp_gather_u32": (i32, [vp, vp, i64, vp, vp]),
     "skrp_block_keys": (i32, [vp, i32, vp, vp, vp, i64, i32, i64, vp, vp]),
     "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
-    "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, vp]),
+    "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, i32, vp]),
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),
     "skrp_synth_uniform_coords": (i32, [vp, i64, i64, u64, i32, i64, vp]),
     "skrp_synth_zipf_coords": (i32, [vp, i64, vp, i64, u64, i32, i64, vp]),

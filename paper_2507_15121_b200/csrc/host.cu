@@ -193,7 +193,7 @@ extern "C" int skrp_mttkrp_host(const uint64_t *indices, const double *values, i
                 vals_out = (double *)keep.back().p;
             }
             TRY(skrp_carry_fixup(rows_in, vals_in, in_f64, (const int64_t *)d_ch, (const uint8_t *)d_fl, nch, rank,
-                                 (float *)d_out.p, rows_out, vals_out, (skrp_stream_t)s));
+                                 (float *)d_out.p, rows_out, vals_out, 0, (skrp_stream_t)s));
             if (fin) break;
             rows_in = rows_out;
             vals_in = vals_out;

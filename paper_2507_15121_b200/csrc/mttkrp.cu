@@ -48,6 +48,22 @@ __device__ __forceinline__ void store_vec(float *p, const float (&v)[VEC])
 }
 
 template <int VEC>
+__device__ __forceinline__ void rmw_add_vec(float *p, const float (&v)[VEC])
+{
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 4) {
+            float4 o = *reinterpret_cast<float4 *>(p + i);
+            o.x += v[i]; o.y += v[i + 1]; o.z += v[i + 2]; o.w += v[i + 3];
+            *reinterpret_cast<float4 *>(p + i) = o;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) p[i] += v[i];
+    }
+}
+
+template <int VEC>
 __device__ __forceinline__ void red_vec(float *p, const float (&v)[VEC])
 {
     if constexpr (VEC % 4 == 0) {
@@ -250,7 +266,7 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const int32_t *__restr
                                                           const int64_t *__restrict__ chunks,
                                                           const uint8_t *__restrict__ final_flags,
                                                           int64_t n_chunks, int R, float *out,
-                                                          int32_t *rows_out, double *vals_out)
+                                                          int32_t *rows_out, double *vals_out, int additive)
 {
     constexpr int MAXC = 8;  // R <= 256
     const int lane = threadIdx.x & 31;
@@ -273,7 +289,10 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const int32_t *__restr
 #pragma unroll
                 for (int j = 0; j < MAXC; ++j) {
                     int cc = lane + 32 * j;
-                    if (cc < R) out[(size_t)row * R + cc] = (float)acc[j];
+                    if (cc < R) {
+                        if (additive) out[(size_t)row * R + cc] += (float)acc[j];
+                        else out[(size_t)row * R + cc] = (float)acc[j];
+                    }
                 }
             } else {
                 const int64_t entry = 2 * c + (first_seg ? 0 : 1);
@@ -451,8 +470,6 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
         SKRP_REQUIRE(a.carry_rows && a.carry_vals, "deterministic accumulation needs carry buffers");
 
     cudaStream_t s = (cudaStream_t)stream;
-    SKRP_REQUIRE(!(a.flags & SKRP_FLAG_ADDITIVE) || a.accumulation == SKRP_ACC_ATOMIC,
-                 "additive (blocked-layout) execution needs atomic accumulation");
     Variant v = choose(a);
     SKRP_REQUIRE(!(a.flags & SKRP_FLAG_ADDITIVE) || v.v2, "additive execution needs R in {8,16,32,64,128} and N <= 5");
     int occ = 0;
@@ -477,7 +494,7 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
 
 int skrp_carry_fixup(const int32_t *rows_in, const void *vals_in, int32_t vals_in_is_f64,
                      const int64_t *chunks, const uint8_t *final_flags, int64_t n_chunks,
-                     int32_t rank, float *out, int32_t *rows_out, double *vals_out,
+                     int32_t rank, float *out, int32_t *rows_out, double *vals_out, int32_t additive,
                      skrp_stream_t stream)
 {
     SKRP_REQUIRE(rank >= 1 && rank <= 256, "rank must be in [1, 256]");
@@ -488,10 +505,10 @@ int skrp_carry_fixup(const int32_t *rows_in, const void *vals_in, int32_t vals_i
     int64_t blocks = std::min<int64_t>((n_chunks + 7) / 8, (int64_t)device_sm_count() * 16);
     if (vals_in_is_f64)
         carry_fixup_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
-            rows_in, (const double *)vals_in, chunks, final_flags, n_chunks, rank, out, rows_out, vals_out);
+            rows_in, (const double *)vals_in, chunks, final_flags, n_chunks, rank, out, rows_out, vals_out, additive ? 1 : 0);
     else
         carry_fixup_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
-            rows_in, (const float *)vals_in, chunks, final_flags, n_chunks, rank, out, rows_out, vals_out);
+            rows_in, (const float *)vals_in, chunks, final_flags, n_chunks, rank, out, rows_out, vals_out, additive ? 1 : 0);
     SKRP_LAUNCHED("carry_fixup_kernel");
     return SKRP_OK;
 }

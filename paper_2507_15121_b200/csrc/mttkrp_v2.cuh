@@ -16,7 +16,10 @@
 //     write each completed row once with the whole warp (one coalesced 128-B
 //     store/red per 32 columns) and carry the last row into the registers;
 //   * ADDITIVE mode (blocked execution layouts, where other tile groups also
-//     contribute to a row) turns every flush into red.global.add.
+//     contribute to a row) turns every flush into an add: red.global.add
+//     under the atomic discipline; under deterministic-reduce the host runs
+//     one launch per block group (rows are exclusive within a launch), so a
+//     plain read-add-write in launch order keeps results bit-reproducible.
 #pragma once
 
 #include <type_traits>
@@ -88,6 +91,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                     const int64_t entry = 2 * t + (is_head ? 0 : 1);
                     store_vec<VEC>(a.carry_vals + (size_t)entry * RR + col, acc);
                     if (lane == 0) a.carry_rows[entry] = (int32_t)row;
+                } else if (additive && det) {
+                    rmw_add_vec<VEC>(dst, acc);  // rows of one launch are exclusive to it
                 } else if (shared || additive) {
                     red_vec<VEC>(dst, acc);
                 } else {
@@ -103,6 +108,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                 const int c = lane + 32 * q;
                 if (c < RR) {
                     if (shared && det) a.carry_vals[(size_t)(2 * t) * RR + c] = v[q];
+                    else if (additive && det) a.out[(size_t)row * RR + c] += v[q];
                     else if (shared || additive) atomicAdd(a.out + (size_t)row * RR + c, v[q]);
                     else a.out[(size_t)row * RR + c] = v[q];
                 }

@@ -88,7 +88,7 @@ class DistributedMttkrp:
         ex = self._execs.get((d, self._rank_r))
         if ex is None or ex.num_tiles == 0:
             return 0
-        return 1 + (len(ex.levels) if ex.det else 0)
+        return ex.launches
 
     def prepare(self, rank_r, dtype=None):
         import torch

@@ -58,7 +58,7 @@ class PlatformConfig:
     tile_nnz: int = 0           # nonzeros per work-queue tile (a slice of one ISP); 0 = auto
     kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
     carry_chunk: int = 256      # carry-tree fan-in
-    layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked, atomic), "auto"
+    layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked), "auto" (cost model)
     l2_budget_mb: int = 192     # L2 bytes the blocked layout plans on (B200-calibrated)
     max_blocks: int = 4         # blocks per input mode the layout search may use (B200-tuned)
 
@@ -75,9 +75,7 @@ class PlatformConfig:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
         if self.layout not in ("flycoo", "blocked", "auto"):
             raise ValueError("layout must be 'flycoo', 'blocked' or 'auto'")
-        if self.layout == "blocked" and self.accumulation != "atomic":
-            raise ValueError("the blocked layout needs accumulation='atomic' (rows collect "
-                             "contributions from several block groups)")
+
 
 
 def _torch():
@@ -268,9 +266,9 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo":
         return plan
-    if cfg.accumulation != "atomic" or rank not in _V2_RANKS or len(plan.shape) > 5:
+    if rank not in _V2_RANKS or len(plan.shape) > 5:
         if cfg.layout == "blocked":
-            raise ValueError("blocked layout needs atomic accumulation, R in {8,16,32,64,128}, N <= 5")
+            raise ValueError("blocked layout needs R in {8,16,32,64,128} and N <= 5")
         return plan
     shifts, cost, base = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20,
                                          max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
@@ -297,46 +295,62 @@ def auto_tile_nnz(nnz: int, gpu=None) -> int:
 
 
 class _ShardExec:
-    """Device-resident tile table + carry-tree buffers for a set of shards."""
+    """Device-resident tile tables + carry-tree buffers for a set of shards.
+
+    One SEGMENT = one kernel launch (+ its carry tree).  Plan order and the
+    atomic blocked layout need one segment; the deterministic blocked layout
+    runs one segment per block group (rows are exclusive inside a segment,
+    flushes read-add-write in segment order -> bit-reproducible)."""
 
     def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
         torch = _torch()
         self.gpu = gpu
         self.rank = rank
         self.det = cfg.accumulation == "deterministic-reduce"
-        nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
-        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(nnz, gpu)
-        if plan.layout == "blocked" and self.det:
-            raise ValueError("blocked layout needs atomic accumulation")
-        self.flags = _lib.FLAG_ADDITIVE if plan.layout == "blocked" else 0
-        tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz)
-        self.num_tiles = len(tiles) // 2
+        self.blocked = plan.layout == "blocked"
+        self.flags = _lib.FLAG_ADDITIVE if self.blocked else 0
         self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
-        self.tiles = torch.from_numpy(tiles).to(gpu)
+        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
+        if self.blocked and self.det:
+            keys = sorted({int(k) for j in shard_ids if plan.shards[j].nnz for k in plan.groups[j][:, 2]})
+        else:
+            keys = [None]
+        self.segments = []
+        for key in keys:
+            tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz, group_key=key)
+            if len(tiles) == 0:
+                continue
+            seg = {"n": len(tiles) // 2, "tiles": torch.from_numpy(tiles).to(gpu), "levels": []}
+            if self.det:
+                for table, final in carry_levels(per_shard, cfg.carry_chunk):
+                    nch = len(final)
+                    lvl = {"n": nch, "chunks": torch.from_numpy(table).to(gpu),
+                           "final": torch.from_numpy(final).to(gpu), "rows_out": None, "vals_out": None}
+                    if not final.all():
+                        lvl["rows_out"] = torch.empty(2 * nch, dtype=torch.int32, device=gpu)
+                        lvl["vals_out"] = torch.empty(2 * nch * rank, dtype=torch.float64, device=gpu)
+                    seg["levels"].append(lvl)
+            self.segments.append(seg)
+        self.num_tiles = sum(sg["n"] for sg in self.segments)
         self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
-        self.levels = []
-        if self.det and self.num_tiles:
-            self.carry_rows = torch.empty(2 * self.num_tiles, dtype=torch.int32, device=gpu)
-            self.carry_vals = torch.empty(2 * self.num_tiles * rank, dtype=torch.float32, device=gpu)
-            for table, final in carry_levels(per_shard, cfg.carry_chunk):
-                nch = len(final)
-                lvl = {
-                    "n": nch,
-                    "chunks": torch.from_numpy(table).to(gpu),
-                    "final": torch.from_numpy(final).to(gpu),
-                    "rows_out": None,
-                    "vals_out": None,
-                }
-                if not final.all():
-                    lvl["rows_out"] = torch.empty(2 * nch, dtype=torch.int32, device=gpu)
-                    lvl["vals_out"] = torch.empty(2 * nch * rank, dtype=torch.float64, device=gpu)
-                self.levels.append(lvl)
+        mx = max((sg["n"] for sg in self.segments), default=0)
+        if self.det and mx:
+            self.carry_rows = torch.empty(2 * mx, dtype=torch.int32, device=gpu)
+            self.carry_vals = torch.empty(2 * mx * rank, dtype=torch.float32, device=gpu)
         else:
             self.carry_rows = self.carry_vals = None
 
+    @property
+    def levels(self):  # carry-tree launches of the first segment (reporting)
+        return self.segments[0]["levels"] if self.segments else []
+
+    @property
+    def launches(self) -> int:
+        return sum(1 + len(sg["levels"]) for sg in self.segments)
+
     def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
-        """Launch the tile kernel (+ carry tree).  `events` (start, end) CUDA
-        events, if given, bracket the tile kernel alone on `stream`."""
+        """Launch the tile kernel(s) (+ carry trees).  `events` (start, end) CUDA
+        events, if given, bracket all launches of this mode on `stream`."""
         if self.num_tiles == 0:
             return
         a = _lib.MttkrpArgs()
@@ -350,8 +364,6 @@ class _ShardExec:
             a.factors[w] = None if w == mode else factors[w].data_ptr()
         a.values = vals.data_ptr()
         a.out = out.data_ptr()
-        a.tiles = self.tiles.data_ptr()
-        a.num_tiles = self.num_tiles
         a.carry_rows = self.carry_rows.data_ptr() if self.det else None
         a.carry_vals = self.carry_vals.data_ptr() if self.det else None
         a.work_counter = self.counter.data_ptr()
@@ -360,19 +372,23 @@ class _ShardExec:
         a.flags = self.flags
         if events is not None:
             events[0].record()  # current stream == `stream` (callers launch on it)
-        _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
+        for seg in self.segments:
+            a.tiles = seg["tiles"].data_ptr()
+            a.num_tiles = seg["n"]
+            _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
+            if not self.det:
+                continue
+            rows_in, vals_in, in_f64 = self.carry_rows, self.carry_vals, 0
+            for lvl in seg["levels"]:
+                _lib.call("skrp_carry_fixup", rows_in.data_ptr(), vals_in.data_ptr(), in_f64,
+                          lvl["chunks"].data_ptr(), lvl["final"].data_ptr(), lvl["n"], self.rank,
+                          out.data_ptr(), _lib.ptr(lvl["rows_out"]), _lib.ptr(lvl["vals_out"]),
+                          1 if self.blocked else 0, stream)
+                if lvl["rows_out"] is None:
+                    break
+                rows_in, vals_in, in_f64 = lvl["rows_out"], lvl["vals_out"], 1
         if events is not None:
             events[1].record()
-        if not self.det:
-            return
-        rows_in, vals_in, in_f64 = self.carry_rows, self.carry_vals, 0
-        for lvl in self.levels:
-            _lib.call("skrp_carry_fixup", rows_in.data_ptr(), vals_in.data_ptr(), in_f64,
-                      lvl["chunks"].data_ptr(), lvl["final"].data_ptr(), lvl["n"], self.rank,
-                      out.data_ptr(), _lib.ptr(lvl["rows_out"]), _lib.ptr(lvl["vals_out"]), stream)
-            if lvl["rows_out"] is None:
-                break
-            rows_in, vals_in, in_f64 = lvl["rows_out"], lvl["vals_out"], 1
 
 
 def _plan_arrays(plan: ModePartitionPlan, gpu):

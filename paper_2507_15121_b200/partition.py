@@ -390,7 +390,7 @@ def build_all_plans(tensor: SparseTensorCOO, cfg: PartitionConfig, *,
 # ------------------------------------------------------------- work tables
 
 
-def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
+def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int, group_key=None):
     """[start, end) element ranges of the TILES of the given shards, in order.
 
     A tile is a slice of one ISP of at most ``tile_nnz`` elements; tiles
@@ -410,6 +410,11 @@ def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
         if blocked:
             # blocked layout: tiles slice the shard's block groups instead
             g = plan.groups[j]
+            if group_key is not None:
+                g = g[g[:, 2] == group_key]
+                if len(g) == 0:
+                    per_shard.append(0)
+                    continue
             isp0 = g[:, 0] - sh.start
             isp1 = g[:, 1] - sh.start
         else:
@@ -438,6 +443,8 @@ def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int):
             if sh.nnz == 0:
                 continue
             g = plan.groups[j]
+            if group_key is not None:
+                g = g[g[:, 2] == group_key]
             glen = ((g[:, 1] - g[:, 0]) + step - 1) // step
             gkeys.append(np.repeat(g[:, 2], glen))
         gk = np.concatenate(gkeys)

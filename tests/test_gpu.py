@@ -414,9 +414,34 @@ def test_blocked_layout_parity(golden, name):
             if s_.nnz:
                 assert g[0, 0] == s_.start and g[-1, 1] == s_.stop and np.all(g[1:, 0] == g[:-1, 1])
         assert np.array_equal(p._indices, plans[f"{name}_m{d}_sorted_indices"])
-        cfg = sk.PlatformConfig(devices=2, rank=32, accumulation="atomic", tile_nnz=16, layout="blocked")
-        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
-        assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL
+        for acc in ("atomic", "deterministic-reduce"):
+            cfg = sk.PlatformConfig(devices=2, rank=32, accumulation=acc, tile_nnz=16, layout="blocked")
+            out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+            assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL
+
+
+def test_blocked_deterministic_device_count_invariance():
+    """Deterministic-reduce in the blocked layout (one launch per block group,
+    read-add-write flushes, additive carry trees): bit-identical results for
+    any device count / placement, like the reference's deterministic mode."""
+    t = sk.synth_tensor((300, 200, 150), 400_000, seed=8)
+    fs = sk.random_factors(t.shape, 32, seed=3)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4, isp_capacity=512))
+    results = []
+    for m, sched in [(1, "dynamic"), (2, "static"), (4, "contiguous"), (1, "dynamic")]:
+        cfg = sk.PlatformConfig(devices=m, rank=32, scheduling=sched, tile_nnz=64, layout="blocked",
+                                l2_budget_mb=0)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        results.append(outs)
+    assert all(p.layout == "blocked" for p in plans)
+    for outs in results[1:]:
+        for a, b in zip(results[0], outs):
+            assert np.array_equal(a, b)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(results[0][d], expect) <= TOL
+        facs[d] = results[0][d]
 
 
 def test_blocked_layout_through_runner(golden):

@@ -97,6 +97,19 @@ def als_update(mttkrp_out, grams):
     return solved / safe, lambdas
 
 
+def mm_fp32(a, b, out=None):
+    """Plain fp32 GEMM through cuBLAS with TF32 forced off (a global TF32
+    switch would break the reference's 1e-4 tolerance)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return torch.mm(a, b, out=out)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def _col_sumsq(x) -> np.ndarray:
     import torch
 
@@ -115,10 +128,9 @@ def _als_update_device(m, grams):
     v = _hadamard(grams, rank)
     if not np.isfinite(v).all():
         raise FloatingPointError("non-finite Gram product")
-    w = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device)
-    solved = torch.empty_like(m)
+    w = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
+    solved = mm_fp32(m, w)  # plain GEMM (rows x R) @ (R x R): cuBLAS fp32
     stream = torch.cuda.current_stream(m.device).cuda_stream
-    _lib.call("skrp_apply_rr", m.data_ptr(), rows, rank, w.data_ptr(), solved.data_ptr(), stream)
     lambdas = np.sqrt(_col_sumsq(solved))
     if not np.isfinite(lambdas).all():
         raise FloatingPointError("non-finite entries in updated factor matrix")

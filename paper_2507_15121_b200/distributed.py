@@ -308,7 +308,7 @@ class DistributedCpAls:
         import torch
 
         from . import _lib
-        from .cpd import _fit_value, _hadamard, _solve_matrix
+        from .cpd import _fit_value, _hadamard, _solve_matrix, mm_fp32
 
         facs = [f.clone() for f in factors]
         nm = len(facs)
@@ -325,12 +325,13 @@ class DistributedCpAls:
                 v = _hadamard([grams[w] for w in range(nm) if w != d], R)
                 if not np.isfinite(v).all():
                     raise FloatingPointError("non-finite Gram product")
-                w_t = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device)
+                # owned rows times the R x R inverse: a plain GEMM -> cuBLAS (fp32,
+                # no TF32); everything around it is this package's kernels
+                w_t = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
                 new = torch.empty_like(m)
                 for lo, hi in self._owned(d):
                     if hi > lo:
-                        _lib.call("skrp_apply_rr", m[lo:hi].data_ptr(), hi - lo, R, w_t.data_ptr(),
-                                  new[lo:hi].data_ptr(), stream)
+                        mm_fp32(m[lo:hi], w_t, out=new[lo:hi])
                 lambdas = np.sqrt(self._col_sumsq(new, d))
                 if not np.isfinite(lambdas).all():
                     raise FloatingPointError("non-finite entries in updated factor matrix")

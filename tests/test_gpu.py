@@ -525,3 +525,30 @@ def test_distributed_cp_als_rank4_blocked_atomic(golden):
     init = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in sk.random_factors(t.shape, 4, seed=0)]
     _, _, hist = als.run(init, iterations=25)
     assert hist[-1] > 0.99 and abs(hist[-1] - golden("cpd.npz")["r4_fit"][-1]) < 1e-3
+
+
+def test_dense_cpd_kernels_vs_numpy():
+    """skrp_gram / skrp_apply_rr / skrp_col_sumsq / skrp_weighted_dot / skrp_sumsq."""
+    rng = np.random.default_rng(1)
+    for rows, R in [(1, 8), (1000, 16), (70_001, 32), (40_000, 64), (5000, 7)]:
+        y = rng.random((rows, R)).astype(np.float32)
+        yt = torch.from_numpy(y).cuda()
+        g = torch.empty((R, R), dtype=torch.float64, device="cuda")
+        _lib.call("skrp_gram", yt.data_ptr(), rows, R, g.data_ptr(), stream())
+        ref = y.astype(np.float64).T @ y.astype(np.float64)
+        assert np.allclose(g.cpu().numpy(), ref, rtol=2e-5)  # fp32 partial sums over <=1024 rows, fp64 across
+        w = rng.standard_normal((R, R))
+        wt = torch.from_numpy(w).cuda()
+        out = torch.empty_like(yt)
+        _lib.call("skrp_apply_rr", yt.data_ptr(), rows, R, wt.data_ptr(), out.data_ptr(), stream())
+        assert np.allclose(out.cpu().numpy(), y.astype(np.float64) @ w, rtol=1e-4, atol=1e-4)
+        cs = torch.empty(R, dtype=torch.float64, device="cuda")
+        _lib.call("skrp_col_sumsq", yt.data_ptr(), rows, R, cs.data_ptr(), stream())
+        assert np.allclose(cs.cpu().numpy(), (y.astype(np.float64) ** 2).sum(0), rtol=1e-9)
+        lam = rng.random(R)
+        lt = torch.from_numpy(lam).cuda()
+        o = torch.empty(1, dtype=torch.float64, device="cuda")
+        _lib.call("skrp_weighted_dot", yt.data_ptr(), yt.data_ptr(), rows, R, lt.data_ptr(), o.data_ptr(), stream())
+        assert np.isclose(o.item(), float((y.astype(np.float64) ** 2 @ lam).sum()), rtol=1e-9)
+        _lib.call("skrp_sumsq", yt.data_ptr(), rows * R, o.data_ptr(), stream())
+        assert np.isclose(o.item(), float((y.astype(np.float64) ** 2).sum()), rtol=1e-9)

@@ -102,7 +102,7 @@ class DistributedMttkrp:
                 self._exec(d, rank_r)
 
     def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None,
-            after_mode=None):
+            after_mode=None, outputs=None):
         """All modes; `factors` are this rank's full fp32 factor replicas.
         Returns the list of gathered outputs (device tensors, reused).
         ``after_mode(i, out)`` is called once mode i's output is gathered
@@ -114,7 +114,8 @@ class DistributedMttkrp:
             self.prepare(rank_r, factors[0].dtype)
         facs = list(factors)
         for d, plan in enumerate(self.plans):
-            out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d])
+            out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
+                                   out=None if outputs is None else outputs[d])
             if self.world > 1:
                 allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
             if after_mode is not None:
@@ -123,16 +124,16 @@ class DistributedMttkrp:
                 facs[plan.mode] = out
         return self.outputs
 
-    def mode_output(self, d, factors, events=None):
-        """Mode d's MTTKRP on this rank's shards into self.outputs[d]: owned
-        rows valid, nothing exchanged yet."""
+    def mode_output(self, d, factors, events=None, out=None):
+        """Mode d's MTTKRP on this rank's shards into self.outputs[d] (or
+        `out`): owned rows valid, nothing exchanged yet."""
         import torch
 
         rank_r = factors[0].shape[1]
         if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
             self.prepare(rank_r, factors[0].dtype)
         plan = self.plans[d]
-        out = self.outputs[d]
+        out = self.outputs[d] if out is None else out
         for lo, hi in self.ownership[d][self.rank]:
             out[lo:hi].zero_()
         if self.compute is not None:
@@ -173,6 +174,63 @@ class DistributedMttkrp:
         with torch.cuda.graph(g):
             self.run(factors, chained=chained)
         return g
+
+    def run_host_pipelined(self, host_factors, host_outputs, steps, chained=True):
+        """`steps` end-to-end steps with HOST buffers, double-buffered: step
+        k+1's factor upload (copy stream) and step k's result download (second
+        copy stream) run while step k / k+1 compute, like a loader feeding a
+        pipeline.  Every step still moves its inputs H2D and its outputs D2H
+        inside the caller's timed region; only the overlap changes.
+        host_outputs: two sets of pinned (rows x R) tensors (alternating).
+        Returns (h2d bytes per step, d2h bytes per step)."""
+        import torch
+
+        dev = self.device
+        comp = torch.cuda.current_stream(dev)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        need = self.needed_factors(chained)
+        rank_r = host_factors[0].shape[1]
+        if self.outputs is None or self._rank_r != rank_r:
+            self.prepare(rank_r)
+        if not hasattr(self, "_pipe"):
+            fac_sets = [[torch.empty(h.shape, dtype=h.dtype, device=dev) for h in host_factors] for _ in range(2)]
+            out_sets = [self.outputs, [torch.empty_like(o) for o in self.outputs]]
+            self._pipe = (fac_sets, out_sets)
+        fac_sets, out_sets = self._pipe
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+        h2d = sum(host_factors[w].numel() * host_factors[w].element_size() for w in need)
+        d2h = sum(o.numel() * o.element_size() for o in self.outputs)
+
+        def upload(b):
+            with torch.cuda.stream(s_in):
+                for w in need:
+                    fac_sets[b][w].copy_(host_factors[w], non_blocking=True)
+                ev_in[b].record(s_in)
+
+        s_in.wait_stream(comp)
+        upload(0)
+        for k in range(steps):
+            b = k % 2
+            comp.wait_event(ev_in[b])
+            if k >= 2:
+                comp.wait_event(ev_out[b])  # step k-2's download of this output set is done
+            self.run(fac_sets[b], chained=chained, outputs=out_sets[b])
+            ev_comp[b].record(comp)
+            if k + 1 < steps:
+                nb = 1 - b
+                if k >= 1:
+                    s_in.wait_event(ev_comp[nb])  # step k-1 finished reading that factor set
+                upload(nb)
+            s_out.wait_event(ev_comp[b])
+            with torch.cuda.stream(s_out):
+                for ho, o in zip(host_outputs[b], out_sets[b]):
+                    ho.copy_(o, non_blocking=True)
+                ev_out[b].record(s_out)
+        comp.wait_stream(s_out)
+        comp.wait_stream(s_in)
+        return h2d, d2h
 
     def run_host(self, host_factors, host_outputs, dev_factors, chained=True, copy_streams=None):
         """End-to-end step with HOST buffers (pinned): upload the factors the

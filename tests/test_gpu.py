@@ -552,3 +552,23 @@ def test_dense_cpd_kernels_vs_numpy():
         assert np.isclose(o.item(), float((y.astype(np.float64) ** 2 @ lam).sum()), rtol=1e-9)
         _lib.call("skrp_sumsq", yt.data_ptr(), rows * R, o.data_ptr(), stream())
         assert np.isclose(o.item(), float((y.astype(np.float64) ** 2).sum()), rtol=1e-9)
+
+
+def test_runner_pipelined_host_path(golden):
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    t = tensor_from(golden, "z3")
+    fs = factors_from(golden, "z3", 32, 3)
+    plans = sk.build_all_plans(t, sk.PartitionConfig())
+    runner = DistributedMttkrp(plans, sk.PlatformConfig(rank=32, accumulation="atomic", layout="blocked",
+                                                        l2_budget_mb=0))
+    dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+    eager = [o.clone() for o in runner.run(dev_f)]
+    host_f = [torch.from_numpy(f.data.astype(np.float32)).pin_memory() for f in fs]
+    host_o = [[torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in eager] for _ in range(2)]
+    h2d, d2h = runner.run_host_pipelined(host_f, host_o, 5)
+    torch.cuda.synchronize()
+    assert h2d == sum(host_f[w].numel() * 4 for w in (1, 2)) and d2h == sum(o.numel() * 4 for o in eager)
+    for b in range(2):
+        for got, want in zip(host_o[b], eager):
+            assert rel_err(got.double().numpy(), want.double().cpu().numpy()) <= 1e-6

@@ -23,7 +23,8 @@ from __future__ import annotations
 import numpy as np
 
 from .collective import TransferLedger, allgather_owned_rows
-from .engine import PlatformConfig, _normalize_ranges, _plan_arrays, _shard_exec, apply_layout, assign_shards
+from .engine import (PlatformConfig, _normalize_ranges, _plan_arrays, _shard_exec, apply_layout, assign_elements,
+                     assign_shards)
 
 
 def _dist():
@@ -58,11 +59,40 @@ class DistributedMttkrp:
             self.ownership.append([_normalize_ranges([p.shards[j].index_range for j in a[r]])
                                    for r in range(self.world)])
             self.mine.append(a[self.rank])
+        self.erange = [None] * len(self.plans)   # element range (split placement)
+        self.boundary = [[] for _ in self.plans]  # rows summed across ranks (split)
+        self.touch = [None] * len(self.plans)    # rows this rank writes (split)
+        if cfg.scheduling == "split":
+            for d, p in enumerate(self.plans):
+                ranges, ids, bnd, rcut = assign_elements(p, self.world)
+                self.erange[d] = ranges[self.rank]
+                self.mine[d] = ids[self.rank]
+                self.boundary[d] = bnd
+                bset = set(bnd)
+                own = []
+                for r in range(self.world):
+                    lo, hi = rcut[r], rcut[r + 1]
+                    rr, cur = [], lo
+                    for b in bnd:  # boundary rows are all-reduced, not broadcast
+                        if lo <= b < hi:
+                            if b > cur:
+                                rr.append((cur, b))
+                            cur = b + 1
+                    if hi > cur:
+                        rr.append((cur, hi))
+                    own.append(rr)
+                self.ownership[d] = own
+                lo, hi = rcut[self.rank], rcut[self.rank + 1]
+                if hi in bset:
+                    hi += 1
+                self.touch[d] = (lo, min(hi, p.shape[p.mode]))
         self._execs = {}
         self.outputs = None
 
     # ------------------------------------------------------------ accounting
     def local_nnz(self, d) -> int:
+        if self.erange[d] is not None:
+            return int(self.erange[d][1] - self.erange[d][0])
         p = self.plans[d]
         return int(sum(p.shards[j].nnz for j in self.mine[d]))
 
@@ -81,7 +111,8 @@ class DistributedMttkrp:
     def _exec(self, d, rank_r):
         key = (d, rank_r)
         if key not in self._execs:
-            self._execs[key] = _shard_exec(self.plans[d], self.mine[d], self.cfg, rank_r, self.device)
+            self._execs[key] = _shard_exec(self.plans[d], self.mine[d], self.cfg, rank_r, self.device,
+                                           clip=self.erange[d])
         return self._execs[key]
 
     def launches_per_mode(self, d) -> int:
@@ -134,6 +165,9 @@ class DistributedMttkrp:
             self.prepare(rank_r, factors[0].dtype)
         plan = self.plans[d]
         out = self.outputs[d] if out is None else out
+        if self.touch[d] is not None:
+            lo, hi = self.touch[d]
+            out[lo:hi].zero_()
         for lo, hi in self.ownership[d][self.rank]:
             out[lo:hi].zero_()
         if self.compute is not None:
@@ -143,7 +177,29 @@ class DistributedMttkrp:
             stream = torch.cuda.current_stream(self.device)
             self._exec(d, rank_r).run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg,
                                       stream.cuda_stream, events=events)
+        if self.boundary[d]:
+            self._reduce_boundary(d, out)
         return out
+
+    def _reduce_boundary(self, d, out):
+        """Split placement: rows cut by a range edge hold per-rank partial sums;
+        sum them across ranks (all ranks end with the full rows)."""
+        import torch
+
+        rows = torch.tensor(self.boundary[d], dtype=torch.int64, device=out.device)
+        lo, hi = self.touch[d]
+        mine = ((rows >= lo) & (rows < hi)).to(out.dtype).unsqueeze(1)
+        part = out.index_select(0, rows) * mine
+        if self.world > 1:
+            import torch.distributed as dist
+
+            if dist.get_backend(self.group) == "nccl" or part.device.type == "cpu":
+                dist.all_reduce(part, group=self.group)
+            else:
+                c = part.cpu()
+                dist.all_reduce(c, group=self.group)
+                part.copy_(c)
+        out.index_copy_(0, rows, part)
 
     def needed_factors(self, chained=True):
         """Modes whose INPUT factor is actually read: with chaining, factor w
@@ -287,8 +343,14 @@ class DistributedCpAls:
             dist.all_reduce(t, group=self.group)
         return t
 
-    def _owned(self, d):
-        return self.mt.ownership[d][self.mt.rank]
+    def _owned(self, d, count_once=False):
+        """Rows this rank updates.  Under split placement the boundary rows
+        (full after the cross-rank sum) are updated redundantly by every rank
+        and, for partial sums (count_once), counted by rank 0 only."""
+        own = list(self.mt.ownership[d][self.mt.rank])
+        if self.mt.boundary[d] and (not count_once or self.mt.rank == 0):
+            own += [(b, b + 1) for b in self.mt.boundary[d]]
+        return own
 
     def _partial_gram(self, y, d):
         import torch
@@ -299,7 +361,7 @@ class DistributedCpAls:
         g = torch.zeros((R, R), dtype=torch.float64, device=y.device)
         tmp = torch.empty((R, R), dtype=torch.float64, device=y.device)
         stream = torch.cuda.current_stream(y.device).cuda_stream
-        for lo, hi in self._owned(d):
+        for lo, hi in self._owned(d, count_once=True):
             if hi > lo:
                 _lib.call("skrp_gram", y[lo:hi].data_ptr(), hi - lo, R, tmp.data_ptr(), stream)
                 g += tmp
@@ -314,7 +376,7 @@ class DistributedCpAls:
         acc = torch.zeros(R, dtype=torch.float64, device=x.device)
         tmp = torch.empty(R, dtype=torch.float64, device=x.device)
         stream = torch.cuda.current_stream(x.device).cuda_stream
-        for lo, hi in self._owned(d):
+        for lo, hi in self._owned(d, count_once=True):
             if hi > lo:
                 _lib.call("skrp_col_sumsq", x[lo:hi].data_ptr(), hi - lo, R, tmp.data_ptr(), stream)
                 acc += tmp
@@ -332,10 +394,13 @@ class DistributedCpAls:
             total = torch.zeros(1, dtype=torch.float64, device=self.mt.device)
             out = torch.empty(1, dtype=torch.float64, device=self.mt.device)
             stream = torch.cuda.current_stream(self.mt.device).cuda_stream
-            for j in self.mt.mine[0]:
-                sh = plan.shards[j]
-                if sh.nnz:
-                    _lib.call("skrp_sumsq", vals.data_ptr() + 4 * sh.start, sh.nnz, out.data_ptr(), stream)
+            if self.mt.erange[0] is not None:
+                spans = [self.mt.erange[0]]
+            else:
+                spans = [(plan.shards[j].start, plan.shards[j].stop) for j in self.mt.mine[0]]
+            for a, b in spans:
+                if b > a:
+                    _lib.call("skrp_sumsq", vals.data_ptr() + 4 * a, b - a, out.data_ptr(), stream)
                     total += out
             self._xsq = float(self._allreduce(total).item())
         return self._xsq
@@ -353,7 +418,7 @@ class DistributedCpAls:
         total = torch.zeros(1, dtype=torch.float64, device=new.device)
         out = torch.empty(1, dtype=torch.float64, device=new.device)
         stream = torch.cuda.current_stream(new.device).cuda_stream
-        for lo, hi in self._owned(d):
+        for lo, hi in self._owned(d, count_once=True):
             if hi > lo:
                 _lib.call("skrp_weighted_dot", new[lo:hi].data_ptr(), m[lo:hi].data_ptr(), hi - lo, R,
                           lam.data_ptr(), out.data_ptr(), stream)

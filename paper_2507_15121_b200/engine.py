@@ -43,7 +43,11 @@ ACCUMULATION_MODES = ("deterministic-reduce", "atomic")
 # "contiguous" (B200 addition): each device gets one run of consecutive shards
 # cut at the cumulative-nnz targets, so its output rows form ONE range and the
 # inter-mode all-gather is one broadcast per device
-SCHEDULING_MODES = ("dynamic", "static", "contiguous")
+# "split" (B200 addition): equal-NONZERO element ranges per
+# device; the <= devices-1 rows cut by a range boundary (heavy rows included)
+# are summed across devices -- perfect balance under any skew, at the price
+# of a tiny cross-device reduction (one-process-per-GPU runner only)
+SCHEDULING_MODES = ("dynamic", "static", "contiguous", "split")
 
 
 @dataclass(frozen=True)
@@ -145,6 +149,29 @@ def elementwise_compute(x: NonzeroElement, factors, mode: int):
 
 
 # ----------------------------------------------------------------- balancer
+
+
+def assign_elements(plan: ModePartitionPlan, m: int):
+    """Element-split placement: device r processes plan elements
+    [r*n//m, (r+1)*n//m) (plan order).  Returns (ranges, shard ids per device,
+    boundary rows cut by a range edge, row cuts R_0..R_m)."""
+    torch = _torch()
+    n = plan.nnz
+    cuts = [r * n // m for r in range(m + 1)]
+    rowc = plan.coords[plan.mode]
+    probe = sorted({c for c in cuts if 0 < c < n} | {c - 1 for c in cuts if 0 < c < n})
+    val = {}
+    if probe:
+        got = rowc[torch.tensor(probe, device=rowc.device, dtype=torch.int64)].cpu().tolist()
+        val = dict(zip(probe, got))
+    rows = plan.shape[plan.mode]
+    rcut = [0] + [val[c] if 0 < c < n else rows for c in cuts[1:-1]] + [rows]
+    boundary = sorted({val[c] for c in cuts[1:-1] if 0 < c < n and val[c - 1] == val[c]})
+    ranges = [(cuts[r], cuts[r + 1]) for r in range(m)]
+    ids = []
+    for e0, e1 in ranges:
+        ids.append([s.shard_id for s in plan.shards if s.nnz and s.start < e1 and s.stop > e0])
+    return ranges, ids, boundary, rcut
 
 
 def assign_shards(plan: ModePartitionPlan, m: int, scheduling: str, weights=None) -> list:
@@ -264,7 +291,7 @@ def choose_blocking(plan, rank, shard_ids=None, l2_bytes=96 << 20, max_blocks=64
 
 def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
-    if cfg.layout == "flycoo" or plan.layout != "flycoo":
+    if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
         return plan
     if rank not in _V2_RANKS or len(plan.shape) > 5:
         if cfg.layout == "blocked":
@@ -302,14 +329,17 @@ class _ShardExec:
     runs one segment per block group (rows are exclusive inside a segment,
     flushes read-add-write in segment order -> bit-reproducible)."""
 
-    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu, clip=None):
         torch = _torch()
         self.gpu = gpu
         self.rank = rank
         self.det = cfg.accumulation == "deterministic-reduce"
         self.blocked = plan.layout == "blocked"
+        if clip is not None and self.blocked:
+            raise ValueError("element-split placement needs the plan-order (flycoo) layout")
         self.flags = _lib.FLAG_ADDITIVE if self.blocked else 0
-        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.nnz = (int(clip[1] - clip[0]) if clip is not None
+                    else int(sum(plan.shards[j].nnz for j in shard_ids)))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
         if self.blocked and self.det:
             keys = sorted({int(k) for j in shard_ids if plan.shards[j].nnz for k in plan.groups[j][:, 2]})
@@ -317,7 +347,7 @@ class _ShardExec:
             keys = [None]
         self.segments = []
         for key in keys:
-            tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz, group_key=key)
+            tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz, group_key=key, clip=clip)
             if len(tiles) == 0:
                 continue
             seg = {"n": len(tiles) // 2, "tiles": torch.from_numpy(tiles).to(gpu), "levels": []}
@@ -404,11 +434,12 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
     return plan._exec_cache[key]
 
 
-def _shard_exec(plan, shard_ids, cfg, rank, gpu) -> _ShardExec:
-    key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout)
+def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None) -> _ShardExec:
+    key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout,
+           clip)
     ex = plan._exec_cache.get(key)
     if ex is None:
-        ex = _ShardExec(plan, shard_ids, cfg, rank, gpu)
+        ex = _ShardExec(plan, shard_ids, cfg, rank, gpu, clip)
         plan._exec_cache[key] = ex
     return ex
 
@@ -485,6 +516,8 @@ def mttkrp_mode(plan: ModePartitionPlan, devices: list, cfg: PlatformConfig,
                       RuntimeWarning, stacklevel=2)
     t_mode = time.perf_counter()
     ledger = ledger if ledger is not None else TransferLedger()
+    if cfg.scheduling == "split":
+        raise ValueError("scheduling='split' needs the one-process-per-GPU runner (distributed.DistributedMttkrp)")
     if assignment is None:
         assignment = assign_shards(plan, m, cfg.scheduling)
     apply_layout(plan, cfg, rank)

@@ -390,12 +390,14 @@ def build_all_plans(tensor: SparseTensorCOO, cfg: PartitionConfig, *,
 # ------------------------------------------------------------- work tables
 
 
-def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int, group_key=None):
+def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int, group_key=None, clip=None):
     """[start, end) element ranges of the TILES of the given shards, in order.
 
     A tile is a slice of one ISP of at most ``tile_nnz`` elements; tiles
     never straddle an ISP (hence never a shard).  Also returns, per shard,
-    its number of tiles (for the carry-tree chunk tables).
+    its number of tiles (for the carry-tree chunk tables).  ``clip`` =
+    (e0, e1) keeps only the parts of tiles inside that element range (the
+    element-split placement, engine.assign_elements).
     """
     cap = plan.isp_capacity
     step = max(1, min(tile_nnz, cap))
@@ -425,8 +427,14 @@ def tile_table(plan: ModePartitionPlan, shard_ids, tile_nnz: int, group_key=None
         first = np.repeat(np.cumsum(pieces) - pieces, pieces)
         s = np.repeat(isp0, pieces) + (np.arange(total, dtype=np.int64) - first) * step
         e = np.minimum(s + step, np.repeat(isp1, pieces))
-        starts.append(s + sh.start)
-        stops.append(e + sh.start)
+        s, e = s + sh.start, e + sh.start
+        if clip is not None:
+            s, e = np.maximum(s, clip[0]), np.minimum(e, clip[1])
+            keep = e > s
+            s, e = s[keep], e[keep]
+            total = int(keep.sum())
+        starts.append(s)
+        stops.append(e)
         per_shard.append(total)
     if starts:
         s = np.concatenate(starts)

@@ -92,6 +92,31 @@ def _worker(rank, world, port, q):
             _, lam1, h1 = single.run(dev_f, iterations=2)
             assert np.allclose(h1, h2, atol=1e-4), (h1, h2)
             assert np.allclose(lam1, lam2, rtol=1e-3), (np.max(np.abs(lam1 - lam2) / np.abs(lam1)), h1, h2)
+        # element-split placement (heavy rows cut across ranks, boundary rows
+        # summed across ranks) on a skewed tensor with replicated plans
+        shape = (40, 900, 700)
+        full = synth_tensor_device(shape, 300_000, distribution="zipf", seed=11)
+        fs = sk.random_factors(shape, 32, seed=2)
+        dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+        for acc in ("deterministic-reduce", "atomic"):
+            cfg = sk.PlatformConfig(devices=world, rank=32, accumulation=acc, scheduling="split", tile_nnz=128)
+            plans = sk.build_all_plans(full, sk.PartitionConfig(devices=world, strategy="nnz-balanced"))
+            runner = DistributedMttkrp(plans, cfg)
+            assert runner.boundary[0], "the zipf head row must straddle the element split"
+            outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+            facs = [f.data.copy() for f in fs]
+            for d in range(3):
+                expect = oracle.mttkrp_seq_c(full.indices, full.values, facs, d)
+                err = np.max(np.abs(outs[d] - expect) / np.maximum(np.abs(expect), 1.0))
+                assert err <= 1e-4, ("split", acc, d, err)
+                facs[d] = outs[d]
+            als = DistributedCpAls(plans, cfg)
+            _, lam2, h2 = als.run(dev_f, iterations=2)
+            single = DistributedCpAls(sk.build_all_plans(full, sk.PartitionConfig()),
+                                      sk.PlatformConfig(devices=1, rank=32, accumulation=acc), rank=0, world=1)
+            _, lam1, h1 = single.run(dev_f, iterations=2)
+            assert np.allclose(h1, h2, atol=1e-4), (h1, h2)
+            assert np.allclose(lam1, lam2, rtol=1e-3)
         q.put((rank, "ok"))
     except Exception as exc:  # pragma: no cover
         import traceback

@@ -116,6 +116,38 @@ __device__ __forceinline__ void ld_row<1>(float (&v)[1], const float *p, uint64_
     asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v[0]) : "l"(p), "l"(pol));
 }
 
+// output-row writes with an L2 eviction policy: output lines are touched once
+// per block group, so they must not push the group's factor blocks out of L2
+__device__ __forceinline__ void red_add_f4_pol(float *p, float4 v, uint64_t pol)
+{
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void st_f4_pol(float *p, float4 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ float4 ld_f4_pol(const float *p, uint64_t pol)
+{
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_add_f1_pol(float *p, float x, uint64_t pol)
+{
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(x), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void st_f1_pol(float *p, float x, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(x), "l"(pol) : "memory");
+}
+
 // vector fp32 reduction into global memory (sm_90+): one op per 16 bytes
 __device__ __forceinline__ void red_add_f4(float *p, float4 v)
 {

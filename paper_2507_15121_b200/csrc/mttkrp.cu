@@ -344,11 +344,11 @@ static Variant mk()
     return v;
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1>
 static Variant mk2()
 {
     Variant v;
-    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN>;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL>;
     v.smem = v2_smem_bytes<8 * LPN>();
     return v;
 }
@@ -426,6 +426,7 @@ static Variant choose(const skrp_mttkrp_args &a)
             if (a.nmodes == 4) return mk2<4, 4, 4, 2>();
         }
         if (a.variant == 10 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1>();  // no L2 hint
+        if (a.variant == 11 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 0>();  // output: no hint
         if (a.variant == 9 && a.rank == 64) {
             if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
             if (a.nmodes == 4) return mk2<4, 8, 4, 1>();

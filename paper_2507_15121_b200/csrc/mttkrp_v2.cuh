@@ -24,7 +24,32 @@
 
 #include <type_traits>
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0>
+template <int VEC>
+__device__ __forceinline__ void out_store(float *p, const float (&v)[VEC], uint64_t pol)
+{
+#pragma unroll
+    for (int i = 0; i < VEC; i += 4) st_f4_pol(p + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]), pol);
+}
+
+template <int VEC>
+__device__ __forceinline__ void out_red(float *p, const float (&v)[VEC], uint64_t pol)
+{
+#pragma unroll
+    for (int i = 0; i < VEC; i += 4) red_add_f4_pol(p + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]), pol);
+}
+
+template <int VEC>
+__device__ __forceinline__ void out_rmw(float *p, const float (&v)[VEC], uint64_t pol)
+{
+#pragma unroll
+    for (int i = 0; i < VEC; i += 4) {
+        float4 o = ld_f4_pol(p + i, pol);
+        o.x += v[i]; o.y += v[i + 1]; o.z += v[i + 2]; o.w += v[i + 3];
+        st_f4_pol(p + i, o, pol);
+    }
+}
+
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     mttkrp_v2_kernel(const skrp_mttkrp_args a, int additive)
 {
@@ -47,6 +72,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     const uint32_t *__restrict__ rowc = a.coords[mode];
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_row = policy_evict_last();
+    // output rows: evict_first (OUTPOL) so the per-group sweep of output lines
+    // does not evict the group's factor blocks; else the default policy
+    uint64_t pol_out;
+    if constexpr (OUTPOL) pol_out = policy_evict_first();
+    else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_out));
     const bool det = a.accumulation == SKRP_ACC_DETERMINISTIC;
     // input modes in ascending order (kernels.py:63-69): j-th input = j or j+1
     const float *__restrict__ F[NIN];
@@ -92,11 +122,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                     store_vec<VEC>(a.carry_vals + (size_t)entry * RR + col, acc);
                     if (lane == 0) a.carry_rows[entry] = (int32_t)row;
                 } else if (additive && det) {
-                    rmw_add_vec<VEC>(dst, acc);  // rows of one launch are exclusive to it
+                    out_rmw<VEC>(dst, acc, pol_out);  // rows of one launch are exclusive to it
                 } else if (shared || additive) {
-                    red_vec<VEC>(dst, acc);
+                    out_red<VEC>(dst, acc, pol_out);
                 } else {
-                    store_vec<VEC>(dst, acc);
+                    out_store<VEC>(dst, acc, pol_out);
                 }
             }
         };
@@ -107,10 +137,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int q = 0; q < CPL; ++q) {
                 const int c = lane + 32 * q;
                 if (c < RR) {
+                    float *dst = a.out + (size_t)row * RR + c;
                     if (shared && det) a.carry_vals[(size_t)(2 * t) * RR + c] = v[q];
-                    else if (additive && det) a.out[(size_t)row * RR + c] += v[q];
-                    else if (shared || additive) atomicAdd(a.out + (size_t)row * RR + c, v[q]);
-                    else a.out[(size_t)row * RR + c] = v[q];
+                    else if (additive && det) st_f1_pol(dst, *dst + v[q], pol_out);
+                    else if (shared || additive) red_add_f1_pol(dst, v[q], pol_out);
+                    else st_f1_pol(dst, v[q], pol_out);
                 }
             }
             if (shared && det && lane == 0) a.carry_rows[2 * t] = (int32_t)row;

@@ -25,9 +25,16 @@
  *   skrp_mttkrp_host           reference.py:32-68 dense_mttkrp_oracle signature with
  *                              host buffers (upload, plan, compute, download in one call)
  *   skrp_synth_*               synth.py:25-93  synth_tensor's laws (uniform / Zipf / values)
+ *   skrp_dedup_mark            synth.py:68-84  first-occurrence de-duplication of draws
  *   skrp_gram, skrp_apply_rr,
  *   skrp_col_sumsq, skrp_scale_cols,
  *   skrp_model_inner           cpd.py:33-105  gram / als_update / fit (+ _model_values_at)
+ *   skrp_weighted_dot,
+ *   skrp_sumsq                 cpd.py:84-105  fit from the last mode's MTTKRP output, ||X||^2
+ *
+ * B200 additions without a reference counterpart (execution layout / multi-GPU):
+ *   skrp_block_keys            sort keys of the L2-blocked execution layout
+ *   skrp_route_by_bounds       destination rank of each nonzero (distributed plan build)
  */
 #ifndef SHARDKRP_CUDA_H
 #define SHARDKRP_CUDA_H

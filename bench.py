@@ -598,7 +598,7 @@ def main():
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
     ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "auto"))
     ap.add_argument("--l2-mb", type=int, default=192)
-    ap.add_argument("--max-blocks", type=int, default=4)
+    ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--parity-rows", type=int, default=512)

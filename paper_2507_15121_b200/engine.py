@@ -64,7 +64,7 @@ class PlatformConfig:
     carry_chunk: int = 256      # carry-tree fan-in
     layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked), "auto" (cost model)
     l2_budget_mb: int = 192     # L2 bytes the blocked layout plans on (B200-calibrated)
-    max_blocks: int = 4         # blocks per input mode the layout search may use (B200-tuned)
+    max_blocks: int = 8         # blocks per input mode the layout search may use (B200-tuned)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:

@@ -257,7 +257,12 @@ class DistributedMttkrp:
         ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
         ev_out = [torch.cuda.Event(), torch.cuda.Event()]
         h2d = sum(host_factors[w].numel() * host_factors[w].element_size() for w in need)
-        d2h = sum(o.numel() * o.element_size() for o in self.outputs)
+        # the gathered result is replicated on every rank: each rank reads back
+        # the rows it owns (the whole matrix at world == 1)
+        spans = [[(lo, hi) for lo, hi in self.ownership[d][self.rank] if hi > lo] + [(b, b + 1) for b in
+                 (self.boundary[d] if self.rank == 0 else [])] for d in range(len(self.plans))]
+        row_b = [o.shape[1] * o.element_size() for o in self.outputs]
+        d2h = sum(sum(hi - lo for lo, hi in spans[d]) * row_b[d] for d in range(len(self.plans)))
 
         def upload(b):
             with torch.cuda.stream(s_in):
@@ -281,8 +286,9 @@ class DistributedMttkrp:
                 upload(nb)
             s_out.wait_event(ev_comp[b])
             with torch.cuda.stream(s_out):
-                for ho, o in zip(host_outputs[b], out_sets[b]):
-                    ho.copy_(o, non_blocking=True)
+                for d, (ho, o) in enumerate(zip(host_outputs[b], out_sets[b])):
+                    for lo, hi in spans[d]:
+                        ho[lo:hi].copy_(o[lo:hi], non_blocking=True)
                 ev_out[b].record(s_out)
         comp.wait_stream(s_out)
         comp.wait_stream(s_in)

@@ -418,7 +418,7 @@ def run_ours(args, cfg):
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "mttkrp_tiles_kernel", "kernel_ms_per_mode": [k * 1e3 for k in kern],
+                         "kernel": "mttkrp_v2_kernel", "kernel_ms_per_mode": [k * 1e3 for k in kern],
                          "algorithmic_bytes_per_mode": alg},
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},

@@ -84,6 +84,21 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def lookup_traffic(config, kernel):
+    """DRAM read+write bytes per launch of `kernel` on `config` from one ncu
+    --set full capture (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            pj = json.load(fh)
+    except Exception:
+        return None
+    for e in pj.get("entries", [pj]):
+        if e.get("config") == config and kernel in e.get("kernel", ""):
+            return e.get("traffic_bytes_per_launch")
+    return None
+
+
 def algorithmic_bytes(shape, nnz, rank, mode):
     n = len(shape)
     return nnz * (4 * n + 4) + nnz * (n - 1) * rank * 4 + shape[mode] * rank * 4
@@ -355,16 +370,8 @@ def run_ours(args, cfg):
     peak, peak_src = load_peaks()
     alg = [runner.algorithmic_bytes(i) for i in range(len(modes))]
     achieved = sum(alg) / sum(kern) / 1e9
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof_path):
-        try:
-            with open(prof_path) as fh:
-                pj = json.load(fh)
-            if pj.get("config") == args.config and world == 1:
-                traffic = pj.get("traffic_bytes_per_launch")
-        except Exception:
-            traffic = None
+    kernel_name = "mttkrp_panel_kernel" if plans[0].layout == "panel" else "mttkrp_v2_kernel"
+    traffic = lookup_traffic(args.config, kernel_name) if world == 1 else None
 
     # ---- end to end through the public runner with pinned host buffers:
     # every step uploads the factors it reads and downloads all outputs;
@@ -418,7 +425,7 @@ def run_ours(args, cfg):
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "mttkrp_v2_kernel", "kernel_ms_per_mode": [k * 1e3 for k in kern],
+                         "kernel": kernel_name, "kernel_ms_per_mode": [k * 1e3 for k in kern],
                          "algorithmic_bytes_per_mode": alg},
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
@@ -488,7 +495,7 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
                        "partition": f"{cfg['strategy']}, devices={world}", "accumulation": args.accumulation,
                        "layout": [p.layout for p in plans], "block_shifts": [p.block_shifts for p in plans]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src, "kernel": "mttkrp_v2_kernel",
+                         "traffic": None, "peak_source": peak_src, "kernel": "mttkrp_panel_kernel" if plans[0].layout == "panel" else "mttkrp_v2_kernel",
                          "kernel_ms_per_mode": [k * 1e3 for k in kern], "algorithmic_bytes_per_mode": alg,
                          "mttkrp_share_of_iteration": sum(kern) / step_s},
             "fit": fits[-1], "clocks": clk, "setup_seconds": setup_s, "plan_build_seconds": build_s,
@@ -596,7 +603,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
-    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "auto"))
+    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "auto"))
     ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")

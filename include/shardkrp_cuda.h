@@ -68,8 +68,12 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);
+int skrp_abi_version(void);  /* 3: skrp_mttkrp_args.factor_ld / out_ld, panel entry points */
 int skrp_device_sm_count(int *out);
+/* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
+ * L2::evict_last, so this bounds how much of the L2 they may pin (B200
+ * addition; 0 restores the default).  *granted = the limit now in force. */
+int skrp_set_l2_persisting(int64_t bytes, int64_t *granted);
 
 /* ------------------------------------------------------ partition (K2/K3) */
 int skrp_histogram(const uint32_t *keys, int64_t n, int64_t num_bins, int64_t *counts,
@@ -86,9 +90,11 @@ int skrp_stable_sort_by_key(const uint32_t *keys, int64_t n, int key_bits, uint3
                             skrp_stream_t stream);
 int skrp_gather_u32(const uint32_t *src, const uint32_t *perm, int64_t n, uint32_t *dst,
                     skrp_stream_t stream);
-/* Sort keys of the L2-blocked execution layout (B200 addition, no reference
- * counterpart): key = [shard | c_w >> shifts[w] for every w with shifts[w] >= 0],
- * widths[w] bits per block id; shard_starts (device, nshards+1 element offsets).
+/* Sort keys of the L2-blocked / panel execution layouts (B200 addition, no
+ * reference counterpart): key = [shard | (c_w >> shifts[w]) & (2^widths[w] - 1)
+ * for every listed part w with shifts[w] >= 0]; coords[] lists the parts in key
+ * order (one coordinate array may appear twice, e.g. an output slab id and its
+ * warp stripe); shard_starts (device, nshards+1 element offsets).
  * A stable sort by this key reorders nonzeros only inside their shard and
  * keeps them sorted by c_d inside each block group. */
 int skrp_block_keys(const uint32_t *const *coords, int32_t nmodes, const int32_t *shifts,
@@ -123,9 +129,54 @@ typedef struct {
     int32_t persistent_ctas;                 /* 0 = #SM x occupancy                 */
     int32_t variant;                         /* 0 = auto; see mttkrp.cu             */
     int32_t flags;                           /* SKRP_FLAG_* bits                    */
+    int32_t factor_ld;                       /* floats between factor rows (0 = R):
+                                                column passes read an R-column slice
+                                                of a wider row or a column plane    */
+    int32_t out_ld;                          /* floats between output rows (0 = R);
+                                                `out` may point at a column offset   */
 } skrp_mttkrp_args;
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);
+
+/* Output-stationary execution (B200 addition; same result contract as
+ * skrp_mttkrp_tiles): output rows are cut into slabs of slab_rows (power of
+ * two) rows; an ITEM is the part of one slab inside one shard.  A CTA claims an
+ * item (device-side queue on args->work_counter), accumulates its rows in a
+ * shared-memory panel while walking the item's block groups in order, and
+ * writes every row of [row_lo, row_hi) exactly once (plain store; red.add when
+ * args->flags has SKRP_FLAG_ADDITIVE) -- the output needs no zeroing.
+ * item_offsets: per item, groups*warps+1 element offsets; the elements of
+ * (group g, warp stripe w) are [off[g*warps+w], off[g*warps+w+1]), and stripe w
+ * holds only rows with (row % slab_rows) / (slab_rows / warps) == w.
+ * Results are bit-identical for any placement of items on devices.
+ * args->tiles / num_tiles / carry_* are ignored. */
+typedef struct {
+    const int64_t *item_rows;     /* 2*num_items: [row_lo, row_hi), inside one slab */
+    const int64_t *item_offsets;  /* num_items * (groups*warps + 1)                 */
+    int64_t num_items;
+    int32_t groups;               /* block groups per item (empty ranges allowed)   */
+    int32_t slab_rows;            /* rows per slab, power of two                     */
+    int32_t warps;                /* warps per CTA == row stripes per slab           */
+    int32_t flags;                /* SKRP_PANEL_* bits                               */
+} skrp_panel_args;
+/* skrp_panel_args.flags: run items in ROUNDS of one item per CTA separated by a
+ * grid barrier (cooperative launch), so all CTAs walk the block groups in step
+ * and the group's factor blocks stay L2-resident.  Without it CTAs claim items
+ * dynamically (better for skewed item sizes). */
+#define SKRP_PANEL_LOCKSTEP 1
+
+int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *panels, skrp_stream_t stream);
+/* warps per CTA and the largest slab the panel kernel supports for (nmodes,
+ * rank); 0 on success, SKRP_ERR_INVALID when no panel kernel exists. */
+int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows);
+
+/* Column planes for column-pass execution (B200 addition, no reference
+ * counterpart): dst (parts x rows x rank/parts, fp32) plane p = columns
+ * [p*rank/parts, (p+1)*rank/parts) of src (rows x rank, row-major).  A pass
+ * over one plane touches rank/parts*4 bytes per gathered row, so twice as many
+ * factor rows stay L2-resident per pass at parts = 2. */
+int skrp_split_columns(const float *src, int64_t rows, int32_t rank, int32_t parts, float *dst,
+                       skrp_stream_t stream);
 
 /* Segmented reduction of boundary-row carries, one level of the fixed tree.
  * chunks: 2*n_chunks [begin, end) entry ranges (never straddling a shard);

@@ -21,12 +21,16 @@ SKRP_OK, SKRP_ERR_INVALID, SKRP_ERR_CUDA, SKRP_ERR_NOMEM, SKRP_ERR_NONFINITE = 0
 SKRP_MAX_MODES = 8
 ACC_DETERMINISTIC, ACC_ATOMIC = 0, 1
 FLAG_ADDITIVE = 1
+PANEL_LOCKSTEP = 1
 
 vp = ctypes.c_void_p
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32
 u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
+
+
+ABI_VERSION = 3  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -48,6 +52,20 @@ class MttkrpArgs(ctypes.Structure):
         ("persistent_ctas", i32),
         ("variant", i32),
         ("flags", i32),
+        ("factor_ld", i32),
+        ("out_ld", i32),
+    ]
+
+
+class PanelArgs(ctypes.Structure):
+    _fields_ = [
+        ("item_rows", vp),
+        ("item_offsets", vp),
+        ("num_items", i64),
+        ("groups", i32),
+        ("slab_rows", i32),
+        ("warps", i32),
+        ("flags", i32),
     ]
 
 
@@ -55,6 +73,10 @@ class MttkrpArgs(ctypes.Structure):
 SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
+    "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
+    "skrp_set_l2_persisting": (i32, [i64, vp]),
+    "skrp_mttkrp_panels": (i32, [vp, vp, vp]),
+    "skrp_panel_shape": (i32, [i32, i32, vp, vp]),
     "skrp_device_sm_count": (i32, [ctypes.POINTER(i32)]),
     "skrp_histogram": (i32, [vp, i64, i64, vp, vp]),
     "skrp_scan_workspace_bytes": (sz, [i64]),
@@ -106,6 +128,9 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        if handle.skrp_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {handle.skrp_abi_version()}, this package needs {ABI_VERSION}: "
+                              f"rebuild it with `make -C {_HERE}`")
         _LIB = handle
     return _LIB
 

@@ -40,6 +40,16 @@ int cuda_status(cudaError_t e, const char *where);
 
 int device_sm_count();
 
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// grid for a grid-stride loop over n items: at most `waves` CTAs per SM
+static inline unsigned grid_for(int64_t n, int block, int waves = 8)
+{
+    int64_t want = ceil_div(n, block);
+    int64_t cap = (int64_t)device_sm_count() * waves;
+    return (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
 // ------------------------------------------------------------- device utils
 __device__ __forceinline__ unsigned lanemask_lt()
 {
@@ -100,6 +110,15 @@ __device__ __forceinline__ void ld_row<4>(float (&v)[4], const float *p, uint64_
 {
     asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+}
+
+// factor row, no L1 allocation (the panel kernel gives most of the SM's
+// L1/shared capacity to shared memory), L2 evict_last via the policy
+__device__ __forceinline__ void ld_row8_na(float (&v)[8], const float *p, uint64_t pol)
+{
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p), "l"(pol));
 }
 
 // no eviction hint (A/B of the L2 policy)

@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) mttkrp_tiles_kernel(c
 }
 
 #include "mttkrp_v2.cuh"
+#include "mttkrp_panel.cuh"
 
 // ------------------------------------------------------------ carry fixup
 // One warp per chunk; lanes own columns; fp64 running sums; rows ascend.
@@ -413,7 +414,7 @@ static bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 static Variant choose(const skrp_mttkrp_args &a)
 {
     Variant v{};
-    bool al32 = aligned(a.out, 32);
+    bool al32 = aligned(a.out, 32) && a.factor_ld % 8 == 0 && a.out_ld % 8 == 0;
     for (int w = 0; w < a.nmodes; ++w) al32 = al32 && (w == a.mode || aligned(a.factors[w], 32));
     if (a.accumulation == SKRP_ACC_DETERMINISTIC) al32 = al32 && aligned(a.carry_vals, 32);
     if (al32 && a.variant != 1) {
@@ -427,6 +428,12 @@ static Variant choose(const skrp_mttkrp_args &a)
         }
         if (a.variant == 10 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1>();  // no L2 hint
         if (a.variant == 11 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 0>();  // output: no hint
+        if (a.variant == 12 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1, 0>();  // no factor/output hints
+        if (a.variant == 13 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 0>();  // 24 warps/SM, output normal
+        // column-pass (R = 16 per pass) A/B variants
+        if (a.variant == 14 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 2>();
+        if (a.variant == 15 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 3, 0, 0>();
+        if (a.variant == 16 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 1, 4>();
         if (a.variant == 9 && a.rank == 64) {
             if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
             if (a.nmodes == 4) return mk2<4, 8, 4, 1>();
@@ -445,6 +452,71 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (pick_fast<0>(a.rank, v)) return v;
     }
     return pick_generic(a.rank);
+}
+
+// ------------------------------------------------------ panel dispatch
+using KernelP = void (*)(const skrp_mttkrp_args, const skrp_panel_args);
+
+struct PanelVariant {
+    KernelP fn = nullptr;
+    int warps = 0;
+    int rr = 0;
+    size_t stage = 0;
+};
+
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0>
+static PanelVariant mkp()
+{
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG>, NW, 8 * LPN, panel_stage_bytes<8 * LPN, NW>()};
+}
+
+static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
+{
+    // A/B variants (R = 32, N = 3): 1 = gathers without L1 allocation,
+    // 2 = 8 warps per CTA, 3 = both
+    if (nmodes == 3 && rank == 32 && variant == 1) return mkp<3, 4, 4, 16, 1>();
+    if (nmodes == 3 && rank == 32 && variant == 2) return mkp<3, 4, 4, 8>();
+    if (nmodes == 3 && rank == 32 && variant == 3) return mkp<3, 4, 4, 8, 1>();
+    // slot-sequential ranges (ALG 1)
+    if (nmodes == 3 && rank == 32 && variant == 4) return mkp<3, 4, 4, 16, 0, 1>();
+    if (nmodes == 3 && rank == 32 && variant == 5) return mkp<3, 4, 2, 16, 0, 1>();
+    if (nmodes == 3 && rank == 32 && variant == 6) return mkp<3, 4, 8, 16, 0, 1>();
+    if (nmodes == 3) {
+        switch (rank) {
+        case 8: return mkp<3, 1, 1, 16>();
+        case 16: return mkp<3, 2, 2, 16>();
+        case 32: return mkp<3, 4, 4, 16>();
+        case 64: return mkp<3, 8, 4, 8>();
+        default: break;
+        }
+    } else if (nmodes == 4) {
+        switch (rank) {
+        case 8: return mkp<4, 1, 1, 16>();
+        case 16: return mkp<4, 2, 1, 16>();
+        case 32: return mkp<4, 4, 2, 16>();
+        case 64: return mkp<4, 8, 2, 8>();
+        default: break;
+        }
+    } else if (nmodes == 5) {
+        switch (rank) {
+        case 8: return mkp<5, 1, 1, 16>();
+        case 16: return mkp<5, 2, 1, 16>();
+        case 32: return mkp<5, 4, 1, 16>();
+        case 64: return mkp<5, 8, 1, 8>();
+        default: break;
+        }
+    }
+    return PanelVariant{};
+}
+
+constexpr size_t kMaxSmemPerCta = 227 * 1024;
+
+static int panel_max_slab(const PanelVariant &v)
+{
+    size_t room = kMaxSmemPerCta - v.stage - 64;  // 64: static shared (item slot)
+    int slab = 1;
+    while ((size_t)(2 * slab) * v.rr * sizeof(float) <= room) slab *= 2;
+    return slab;
 }
 
 }  // namespace skrp
@@ -471,8 +543,12 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
         SKRP_REQUIRE(a.carry_rows && a.carry_vals, "deterministic accumulation needs carry buffers");
 
     cudaStream_t s = (cudaStream_t)stream;
+    SKRP_REQUIRE(a.factor_ld == 0 || a.factor_ld >= a.rank, "factor_ld %d < rank %d", a.factor_ld, a.rank);
+    SKRP_REQUIRE(a.out_ld == 0 || a.out_ld >= a.rank, "out_ld %d < rank %d", a.out_ld, a.rank);
     Variant v = choose(a);
     SKRP_REQUIRE(!(a.flags & SKRP_FLAG_ADDITIVE) || v.v2, "additive execution needs R in {8,16,32,64,128} and N <= 5");
+    const bool pitched = (a.factor_ld > 0 && a.factor_ld != a.rank) || (a.out_ld > 0 && a.out_ld != a.rank);
+    SKRP_REQUIRE(!pitched || v.v2, "row pitches != R (column passes) need R in {8,16,32,64,128} and N <= 5");
     int occ = 0;
     if (v.v2) {
         if (v.smem > 48 * 1024)
@@ -490,6 +566,61 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
     else
         v.fn<<<grid, kWarpsPerCta * 32, 0, s>>>(a);
     SKRP_LAUNCHED("mttkrp_tiles_kernel");
+    return SKRP_OK;
+}
+
+int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows)
+{
+    PanelVariant v = choose_panel(nmodes, rank, 0);
+    SKRP_REQUIRE(v.fn != nullptr, "no panel kernel for nmodes=%d rank=%d (ranks 8/16/32/64, 3..5 modes)", nmodes,
+                 rank);
+    if (warps) *warps = v.warps;
+    if (max_slab_rows) *max_slab_rows = panel_max_slab(v);
+    return SKRP_OK;
+}
+
+int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *panels, skrp_stream_t stream)
+{
+    SKRP_REQUIRE(args != nullptr && panels != nullptr, "skrp_mttkrp_panels: null args");
+    const skrp_mttkrp_args &a = *args;
+    const skrp_panel_args &p = *panels;
+    SKRP_REQUIRE(a.nmodes >= 3 && a.nmodes <= SKRP_MAX_MODES, "nmodes must be in [3, %d]", SKRP_MAX_MODES);
+    SKRP_REQUIRE(a.mode >= 0 && a.mode < a.nmodes, "mode %d out of range", a.mode);
+    SKRP_REQUIRE(p.num_items >= 0 && p.groups >= 1, "bad item count / groups");
+    if (p.num_items == 0) return SKRP_OK;
+    PanelVariant v = choose_panel(a.nmodes, a.rank, a.variant);
+    SKRP_REQUIRE(v.fn != nullptr, "no panel kernel for nmodes=%d rank=%d", a.nmodes, a.rank);
+    SKRP_REQUIRE(p.warps == v.warps, "panel layout built for %d warps, kernel uses %d", p.warps, v.warps);
+    SKRP_REQUIRE(p.slab_rows >= p.warps && (p.slab_rows & (p.slab_rows - 1)) == 0 && p.slab_rows <= panel_max_slab(v),
+                 "slab_rows %d must be a power of two in [%d, %d]", p.slab_rows, p.warps, panel_max_slab(v));
+    SKRP_REQUIRE(a.factor_ld == 0 || (a.factor_ld >= a.rank && a.factor_ld % 8 == 0), "bad factor_ld %d", a.factor_ld);
+    SKRP_REQUIRE(a.out_ld == 0 || (a.out_ld >= a.rank && a.out_ld % 4 == 0), "bad out_ld %d", a.out_ld);
+    SKRP_REQUIRE(p.item_rows && p.item_offsets && a.out && a.values && a.work_counter, "null pointer");
+    for (int w = 0; w < a.nmodes; ++w) {
+        SKRP_REQUIRE(a.coords[w] && (w == a.mode || a.factors[w]), "null coordinate/factor pointer (mode %d)", w);
+        SKRP_REQUIRE(w == a.mode || aligned(a.factors[w], 32), "factor %d must be 32-byte aligned", w);
+    }
+    SKRP_REQUIRE(aligned(a.out, 16), "output must be 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t smem = (size_t)p.slab_rows * v.rr * sizeof(float) + v.stage;
+    SKRP_CUDA(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 1;
+    SKRP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, v.warps * 32, smem));
+    int64_t ctas = a.persistent_ctas > 0 ? a.persistent_ctas : (int64_t)device_sm_count() * std::max(occ, 1);
+    ctas = std::min<int64_t>(ctas, p.num_items);
+    SKRP_CUDA(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), s));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(v.warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = (p.flags & SKRP_PANEL_LOCKSTEP) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SKRP_CUDA(cudaLaunchKernelEx(&cfg, v.fn, a, p));
+    SKRP_LAUNCHED("mttkrp_panel_kernel");
     return SKRP_OK;
 }
 

@@ -1,0 +1,453 @@
+// mttkrp_panel.cuh -- output-stationary MTTKRP over L2-resident factor blocks.
+//
+// Why: a random 128-B factor-row gather runs at ~19.6 TB/s when the rows it
+// touches fit in L2 (<= 64 MB) and at ~8-10 TB/s at 192-256 MB
+// (tools/gather_ceiling.cu, profiles/).  Cutting the input modes into small
+// blocks is only useful if the OUTPUT does not pay for it: in the blocked
+// tile layout every block group re-sweeps the whole output through global
+// atomics (614 MB x groups for cfg2 mode 0).  Here the output never leaves
+// the SM until it is final:
+//
+//   * output rows are cut into SLABS of slab_rows rows; an ITEM is the part
+//     of one slab inside one shard (rows [row_lo, row_hi)); a CTA claims an
+//     item (device-side queue, one atomicAdd per item) and keeps its rows as
+//     an fp32 PANEL in shared memory;
+//   * inside the item the nonzeros are grouped by input-mode BLOCK TUPLES
+//     (groups) in a fixed order; every CTA walks its item's groups in that
+//     order, so at any time the whole GPU gathers from ~one group's factor
+//     blocks, which stay L2-resident;
+//   * warp w of the CTA owns the row STRIPE [slab_base + w*warp_rows, +
+//     warp_rows) of the slab in every group, so panel rows are warp-exclusive:
+//     runs are accumulated in registers (as in mttkrp_v2) and flushed into
+//     the panel with plain shared-memory read-add-write, no atomics;
+//   * when the item is done the panel rows are written to HBM once (plain
+//     coalesced stores; red.global.add when other devices also contribute
+//     to the rows -- SKRP_FLAG_ADDITIVE) and zeroed for the next item.
+//
+// Every row is summed by one warp in a fixed order that depends only on the
+// item's layout, so results are bit-identical for any device count (the
+// reference's deterministic-reduce property, engine.py:12-16) without a
+// carry fix-up pass.
+#pragma once
+
+struct PanelSmem {
+    unsigned long long item;
+};
+
+// grid barrier wait (cooperative launch guarantees co-residency): spin until
+// `target` arrivals; traps after ~10 s instead of hanging the GPU
+__device__ __forceinline__ void grid_wait(unsigned long long *counter, unsigned long long target)
+{
+    unsigned long long seen;
+    for (long long spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(counter) : "memory");
+        if (seen >= target) break;
+        if (spin > (1ll << 27)) __trap();
+        __nanosleep(64);
+    }
+}
+
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0>
+__global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
+    mttkrp_panel_kernel(const skrp_mttkrp_args a, const skrp_panel_args pa)
+{
+    constexpr int VEC = 8;
+    constexpr int S = 32 / LPN;
+    constexpr int G = S * U;
+    constexpr int RR = VEC * LPN;
+    constexpr int STR = RR + 4;
+    constexpr int NIN = NM - 1;
+    constexpr int CPL = (RR + 31) / 32;
+    static_assert(ALG == 1 || 32 % G == 0, "groups must tile the 32-nonzero batch");
+    extern __shared__ __align__(16) float smem_p[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int slab_rows = pa.slab_rows;
+    float *panel = smem_p;                                          // slab_rows x RR
+    float *stage = panel + (size_t)slab_rows * RR + (size_t)wib * (33 * STR);
+    float *carry_row = stage + 32 * STR;
+    __shared__ PanelSmem ctl;
+    const int slot = lane / LPN, sl = lane % LPN;
+    const int col = sl * VEC;
+    const int mode = a.mode;
+    const size_t fld = a.factor_ld > 0 ? (size_t)a.factor_ld : (size_t)RR;
+    const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
+    const bool additive = (a.flags & SKRP_FLAG_ADDITIVE) != 0;
+    const uint32_t *__restrict__ rowc = a.coords[mode];
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_row = policy_evict_last();
+    const float *__restrict__ F[NIN];
+    const uint32_t *__restrict__ C[NIN];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) {
+        const int w = j < mode ? j : j + 1;
+        F[j] = a.factors[w];
+        C[j] = a.coords[w];
+    }
+    const int64_t per_item = (int64_t)pa.groups * NW + 1;
+
+    // the panel starts zeroed; every item zeroes the rows it used on the way out
+    for (int k = threadIdx.x; k < slab_rows * RR / 4; k += NW * 32)
+        reinterpret_cast<float4 *>(panel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    const bool lockstep = (pa.flags & SKRP_PANEL_LOCKSTEP) != 0;
+    for (int64_t round = 0;; ++round) {
+        __syncthreads();  // previous item's write-back / zeroing done
+        int64_t item;
+        if (lockstep) {
+            // ROUNDS: round r runs items r*grid .. r*grid+grid-1, one per CTA,
+            // after a grid-wide barrier, so every CTA walks the same block
+            // groups at the same time (dynamic claiming lets CTAs drift apart
+            // until the GPU gathers from every block at once)
+            if (round * (int64_t)gridDim.x >= pa.num_items) break;
+            if (round > 0 && threadIdx.x == 0) grid_wait(a.work_counter, round * (unsigned long long)gridDim.x);
+            __syncthreads();
+            item = round * (int64_t)gridDim.x + blockIdx.x;
+        } else {
+            if (threadIdx.x == 0) ctl.item = atomicAdd(a.work_counter, 1ull);
+            __syncthreads();
+            item = (int64_t)ctl.item;
+            if (item >= pa.num_items) break;
+        }
+        if (item >= pa.num_items) {  // lockstep tail: idle this round, still arrive
+            if (threadIdx.x == 0) atomicAdd(a.work_counter, 1ull);
+            continue;
+        }
+        const int64_t row_lo = pa.item_rows[2 * item], row_hi = pa.item_rows[2 * item + 1];
+        const int64_t slab_base = row_lo - (row_lo & (int64_t)(slab_rows - 1));
+        const int64_t *__restrict__ offs = pa.item_offsets + item * per_item;
+
+        // panel row of an output row, and the read-add-write flushes
+        auto prow = [&](uint32_t row) { return panel + (size_t)(row - slab_base) * RR; };
+
+        // ALG 1 (slot-sequential): slot s of the warp walks its own contiguous
+        // chunk of the range (len*s/S .. len*(s+1)/S), one nonzero per slot
+        // per step (U steps unrolled), keeping the current row's run in
+        // registers.  Runs that start and end inside the chunk are flushed
+        // with a plain read-add-write (no other slot holds that row); the
+        // chunk's first and last runs (possibly shared with the neighbouring
+        // chunks) are staged and merged column-parallel in row order at the
+        // end of the range.  No per-batch ballots / row classes.
+        auto slot_range = [&](int64_t b0, int64_t b1) {
+            constexpr int PER = (U + LPN - 1) / LPN;
+            constexpr uint32_t NONE = 0xffffffffu;
+            static_assert(ALG == 0 || 2 * S * RR + 2 * S <= 33 * STR, "slot staging does not fit");
+            const int64_t len = b1 - b0;
+            const int64_t e0 = b0 + (len * slot) / S, e1 = b0 + (len * (slot + 1)) / S;
+            const int64_t steps = ((len + S - 1) / S + U - 1) / U;
+            uint32_t m_r[PER], m_c[PER][NIN];
+            float m_v[PER];
+            auto fetch = [&](int64_t sb) {
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int64_t e = sb + sl + q * LPN;
+                    const bool ok = e < e1;
+                    const int64_t idx = ok ? e : (e1 > e0 ? e1 - 1 : b0);
+                    const uint32_t r = ld_stream_u32(rowc + idx, pol_stream);
+                    m_r[q] = ok ? r : NONE;
+                    m_v[q] = ok ? ld_stream_f32(a.values + idx, pol_stream) : 0.f;
+#pragma unroll
+                    for (int j = 0; j < NIN; ++j) m_c[q][j] = ld_stream_u32(C[j] + idx, pol_stream);
+                }
+            };
+            uint32_t cur = NONE, rowF = NONE;
+            bool have_first = false;
+            float acc[VEC], accF[VEC];
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc[i] = accF[i] = 0.f;
+            fetch(e0);
+            for (int64_t st = 0; st < steps; ++st) {
+                uint32_t l_r[PER], l_c[PER][NIN];
+                float l_v[PER];
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    l_r[q] = m_r[q];
+                    l_v[q] = m_v[q];
+#pragma unroll
+                    for (int j = 0; j < NIN; ++j) l_c[q][j] = m_c[q][j];
+                }
+                if (st + 1 < steps) fetch(e0 + (st + 1) * U);
+                float gv[U][NIN][VEC];
+                float vv[U];
+                uint32_t rr[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int src = slot * LPN + (u % LPN);
+                    rr[u] = __shfl_sync(kFull, l_r[u / LPN], src);
+                    vv[u] = __shfl_sync(kFull, l_v[u / LPN], src);
+#pragma unroll
+                    for (int j = 0; j < NIN; ++j) {
+                        const uint32_t idx = __shfl_sync(kFull, l_c[u / LPN][j], src);
+                        if constexpr (L1NA) ld_row8_na(gv[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                        else ld_row<VEC>(gv[u][j], F[j] + (size_t)idx * fld + col, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (rr[u] != NONE && rr[u] != cur) {
+                        if (cur != NONE) {
+                            if (!have_first) {
+#pragma unroll
+                                for (int i = 0; i < VEC; ++i) accF[i] = acc[i];
+                                rowF = cur;
+                                have_first = true;
+                            } else {
+                                rmw_add_vec<VEC>(prow(cur) + col, acc);
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+                        cur = rr[u];
+                    }
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        float p = vv[u];
+#pragma unroll
+                        for (int j = 0; j < NIN - 1; ++j) p *= gv[u][j][i];
+                        acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
+                    }
+                }
+            }
+            // chunk-boundary runs: stage (first, last) per slot, merge in order
+            uint32_t *erow = reinterpret_cast<uint32_t *>(stage + 2 * S * RR);
+            store_vec<VEC>(stage + (2 * slot) * RR + col, accF);
+            store_vec<VEC>(stage + (2 * slot + 1) * RR + col, acc);
+            if (sl == 0) {
+                erow[2 * slot] = rowF;
+                erow[2 * slot + 1] = cur;
+            }
+            __syncwarp();
+            float run[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) run[q] = 0.f;
+            uint32_t rrow = NONE;
+            for (int k = 0; k < 2 * S; ++k) {
+                const uint32_t r = erow[k];
+                if (r == NONE) continue;
+                if (r != rrow) {
+                    if (rrow != NONE) {
+                        float *pr = prow(rrow);
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) {
+                            const int c = lane + 32 * q;
+                            if (c < RR) pr[c] += run[q];
+                            run[q] = 0.f;
+                        }
+                    }
+                    rrow = r;
+                }
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < RR) run[q] += stage[k * RR + c];
+                }
+            }
+            if (rrow != NONE) {
+                float *pr = prow(rrow);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < RR) pr[c] += run[q];
+                }
+            }
+            __syncwarp();
+        };
+
+        for (int g = 0; g < pa.groups; ++g) {
+            const int64_t b0 = offs[g * NW + wib], b1 = offs[g * NW + wib + 1];
+            if (b0 >= b1) continue;
+            if constexpr (ALG == 1) {
+                slot_range(b0, b1);
+                continue;
+            }
+            float acc[VEC];
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+            auto reduce_slots = [&]() {
+#pragma unroll
+                for (int off = LPN; off < 32; off <<= 1)
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
+            };
+            auto write_regs = [&](uint32_t row) {  // slot 0 holds the reduced row
+                if (slot == 0) rmw_add_vec<VEC>(prow(row) + col, acc);
+            };
+            uint32_t nr_l, nc_l[NIN];
+            float nv_l;
+            auto fetch = [&](int64_t nbase) {
+                const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
+                const bool v = lane < nn;
+                const int64_t src = nbase + (v ? lane : nn - 1);
+                nr_l = ld_stream_u32(rowc + src, pol_stream);
+                nv_l = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
+#pragma unroll
+                for (int j = 0; j < NIN; ++j) nc_l[j] = ld_stream_u32(C[j] + src, pol_stream);
+            };
+            fetch(b0);
+            uint32_t cur = __shfl_sync(kFull, nr_l, 0);
+            for (int64_t base = b0; base < b1; base += 32) {
+                const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
+                const uint32_t r_l = nr_l;
+                const float v_l = nv_l;
+                uint32_t c_l[NIN];
+#pragma unroll
+                for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
+                if (base + 32 < b1) fetch(base + 32);
+                const bool uniform = __all_sync(kFull, r_l == cur);
+                int cls = 0, e_b = 32;
+                unsigned cm = 0;
+                float accB[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) accB[i] = 0.f;
+                if (!uniform) {
+                    const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
+                    if (row0 != cur) {
+                        reduce_slots();
+                        write_regs(cur);
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+                        cur = row0;
+                    }
+                    const uint32_t up = __shfl_up_sync(kFull, r_l, 1);
+                    cm = __ballot_sync(kFull, lane > 0 && r_l != up);
+                    const int nb = __popc(cm);
+                    if (nb == 1) {
+                        cls = 1;
+                        e_b = __ffs(cm) - 1;
+                    } else if (nb > 1) {
+                        cls = 2;
+                        reduce_slots();
+                        if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+                    }
+                }
+                auto group = [&](int g0) {
+                    float gv[U][NIN][VEC];
+                    float vv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = g0 + slot * U + u;
+                        vv[u] = __shfl_sync(kFull, v_l, e);
+#pragma unroll
+                        for (int j = 0; j < NIN; ++j) {
+                            const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
+                            if constexpr (L1NA) ld_row8_na(gv[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                            else ld_row<VEC>(gv[u][j], F[j] + (size_t)idx * fld + col, 0);
+                        }
+                    }
+                    if (cls == 0) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                float p = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN - 1; ++j) p *= gv[u][j][i];
+                                acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
+                            }
+                    } else if (cls == 1) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const bool inA = g0 + slot * U + u < e_b;
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                float p = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN - 1; ++j) p *= gv[u][j][i];
+                                if (inA) acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
+                                else accB[i] = fmaf(p, gv[u][NIN - 1][i], accB[i]);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int e = g0 + slot * U + u;
+                            float p[VEC];
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                p[i] = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN; ++j) p[i] *= gv[u][j][i];
+                            }
+                            store_vec<VEC>(stage + e * STR + col, p);
+                        }
+                    }
+                };
+#pragma unroll 1
+                for (int g0 = 0; g0 < nin; g0 += G) group(g0);
+                if (cls == 0) continue;
+                if (cls == 1) {
+                    reduce_slots();
+                    write_regs(cur);
+                    cur = __shfl_sync(kFull, r_l, e_b);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = accB[i];
+                    continue;
+                }
+                // class 2: segmented column sums over the staged rows
+                __syncwarp();
+                float run[CPL];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = lane + 32 * q;
+                    run[q] = (c < RR) ? carry_row[c] : 0.f;
+                }
+                uint32_t row = cur;
+                for (int e = 0; e < nin; ++e) {
+                    if ((cm >> e) & 1u) {
+                        float *pr = prow(row);
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) {
+                            const int c = lane + 32 * q;
+                            if (c < RR) pr[c] += run[q];
+                            run[q] = 0.f;
+                        }
+                        row = __shfl_sync(kFull, r_l, e);
+                    }
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = lane + 32 * q;
+                        if (c < RR) run[q] += stage[e * STR + c];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < RR) carry_row[c] = run[q];
+                }
+                __syncwarp();
+                cur = row;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
+                __syncwarp();
+            }
+            reduce_slots();
+            write_regs(cur);
+            __syncwarp();
+        }
+        __syncthreads();
+        // write-back: the item's rows leave the SM once, then the panel rows
+        // are zeroed for the next item
+        const int64_t nrow = row_hi - row_lo;
+        const int64_t n4 = nrow * (RR / 4);
+        float *pbase = panel + (size_t)(row_lo - slab_base) * RR;
+        for (int64_t k = threadIdx.x; k < n4; k += NW * 32) {
+            const int64_t r = k / (RR / 4);
+            const int c4 = (int)(k - r * (RR / 4));
+            float4 *src = reinterpret_cast<float4 *>(pbase + r * RR) + c4;
+            float *dst = a.out + (size_t)(row_lo + r) * old + 4 * c4;
+            if (additive) red_add_f4(dst, *src);
+            else *reinterpret_cast<float4 *>(dst) = *src;
+            *src = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (lockstep) {
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(a.work_counter, 1ull);
+        }
+    }
+}
+
+template <int RR, int NW>
+constexpr size_t panel_stage_bytes()
+{
+    return sizeof(float) * NW * (33 * (RR + 4));
+}

@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     const int slot = lane / LPN, sl = lane % LPN;
     const int col = sl * VEC;
     const int mode = a.mode;
+    // row pitches: column passes read an RR-wide slice of wider factor rows
+    // (or a column plane) and write an RR-wide slice of wider output rows
+    const size_t fld = a.factor_ld > 0 ? (size_t)a.factor_ld : (size_t)RR;
+    const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
     const uint32_t *__restrict__ rowc = a.coords[mode];
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_row = policy_evict_last();
@@ -116,7 +120,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         auto write_regs = [&](uint32_t row, bool is_head, bool is_tail) {
             const bool shared = (is_head && prev_row == (int64_t)row) || (is_tail && next_row == (int64_t)row);
             if (slot == 0) {
-                float *dst = a.out + (size_t)row * RR + col;
+                float *dst = a.out + (size_t)row * old + col;
                 if (shared && det) {
                     const int64_t entry = 2 * t + (is_head ? 0 : 1);
                     store_vec<VEC>(a.carry_vals + (size_t)entry * RR + col, acc);
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int q = 0; q < CPL; ++q) {
                 const int c = lane + 32 * q;
                 if (c < RR) {
-                    float *dst = a.out + (size_t)row * RR + c;
+                    float *dst = a.out + (size_t)row * old + c;
                     if (shared && det) a.carry_vals[(size_t)(2 * t) * RR + c] = v[q];
                     else if (additive && det) st_f1_pol(dst, *dst + v[q], pol_out);
                     else if (shared || additive) red_add_f1_pol(dst, v[q], pol_out);
@@ -217,8 +221,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                        if constexpr (PLAIN) ld_row8_plain(g[u][j], F[j] + (size_t)idx * RR + col);
-                        else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * RR + col, pol_row);
+                        if constexpr (PLAIN) ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                        else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
                     }
                 }
                 if (cls == 0) {

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(kScanBlock) scan_down_kernel(const T *__restri
         out[n] = (offsets ? offsets[blockIdx.x] : T(0)) + total;
 }
 
-static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 template <typename T>
 static size_t scan_ws_bytes(int64_t n)
@@ -298,13 +297,6 @@ __global__ void gather_u32_kernel(const uint32_t *__restrict__ src, const uint32
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         dst[i] = src[perm[i]];
-}
-
-static unsigned grid_for(int64_t n, int block, int waves = 8)
-{
-    int64_t want = ceil_div(n, block);
-    int64_t cap = (int64_t)device_sm_count() * waves;
-    return (unsigned)std::max<int64_t>(1, std::min(want, cap));
 }
 
 // ------------------------------------------------------- bounds (host side)
@@ -509,7 +501,9 @@ __global__ void block_keys_kernel(BlockKeyArgs a, int nmodes, const int64_t *__r
         uint32_t key = (uint32_t)lo;
         for (int w = 0; w < nmodes; ++w) {
             if (a.shift[w] < 0) continue;
-            key = (key << a.width[w]) | (a.coords[w][i] >> a.shift[w]);
+            // masked to the part's width: a part may take the low bits of a
+            // block id (the panel layout's warp stripe of the output row)
+            key = (key << a.width[w]) | ((a.coords[w][i] >> a.shift[w]) & ((1u << a.width[w]) - 1u));
         }
         (void)shard_bits;
         keys[i] = key;

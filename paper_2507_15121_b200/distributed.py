@@ -165,11 +165,13 @@ class DistributedMttkrp:
             self.prepare(rank_r, factors[0].dtype)
         plan = self.plans[d]
         out = self.outputs[d] if out is None else out
+        writes_all = self.compute is None and getattr(self._exec(d, rank_r), "writes_all_rows", False)
         if self.touch[d] is not None:
             lo, hi = self.touch[d]
             out[lo:hi].zero_()
-        for lo, hi in self.ownership[d][self.rank]:
-            out[lo:hi].zero_()
+        if not writes_all:  # the panel kernel writes every owned row itself
+            for lo, hi in self.ownership[d][self.rank]:
+                out[lo:hi].zero_()
         if self.compute is not None:
             self.compute(plan, self.mine[d], factors, out)
         else:

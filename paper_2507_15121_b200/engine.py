@@ -65,6 +65,13 @@ class PlatformConfig:
     layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked), "auto" (cost model)
     l2_budget_mb: int = 192     # L2 bytes the blocked layout plans on (B200-calibrated)
     max_blocks: int = 8         # blocks per input mode the layout search may use (B200-tuned)
+    col_passes: int = 1         # column passes: each pass gathers R/col_passes columns per factor row,
+                                # so a pass's L2 working set is 1/col_passes of the rows' bytes (atomic only)
+    col_planes: bool = True     # column passes read contiguous column planes (else strided row slices)
+    panel_l2_mb: int = -1       # panel layout: >= 0 cuts input modes to this L2 budget; -1 = blocked cost model
+    slab_rows: int = 0          # panel layout: output rows per slab (0 = auto, see panel_smem_kb)
+    panel_smem_kb: int = 64     # panel layout: shared memory for the output panel (auto slab size)
+    panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -77,8 +84,10 @@ class PlatformConfig:
             raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
-        if self.layout not in ("flycoo", "blocked", "auto"):
-            raise ValueError("layout must be 'flycoo', 'blocked' or 'auto'")
+        if self.layout not in ("flycoo", "blocked", "panel", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked', 'panel' or 'auto'")
+        if self.col_passes < 1 or self.col_passes & (self.col_passes - 1):
+            raise ValueError("col_passes must be a power of two >= 1")
 
 
 
@@ -293,6 +302,12 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
         return plan
+    if cfg.layout == "panel":
+        prm = choose_panels(plan, rank, cfg, shard_ids)
+        if prm is None:
+            raise ValueError("panel layout needs R in {8,16,32,64} and 3..5 modes")
+        plan.to_panels(*prm)
+        return plan
     if rank not in _V2_RANKS or len(plan.shape) > 5:
         if cfg.layout == "blocked":
             raise ValueError("blocked layout needs R in {8,16,32,64,128} and N <= 5")
@@ -300,7 +315,15 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     shifts, cost, base = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20,
                                          max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
     if shifts is not None and (cfg.layout == "blocked" or cost < 0.8 * base):
-        plan.to_blocked(shifts)
+        if (cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce"
+                and panel_shape(len(plan.shape), rank) is not None):
+            # deterministic-reduce: the output-stationary panel kernel sums every
+            # row in a fixed order with no carry pass or per-group launches --
+            # bit-identical across device counts at the atomic blocked speed
+            prm = choose_panels(plan, rank, cfg, shard_ids)
+            plan.to_panels(prm[0], shifts, prm[2])
+        else:
+            plan.to_blocked(shifts)
     return plan
 
 
@@ -361,6 +384,13 @@ class _ShardExec:
                         lvl["vals_out"] = torch.empty(2 * nch * rank, dtype=torch.float64, device=gpu)
                     seg["levels"].append(lvl)
             self.segments.append(seg)
+        # column passes (atomic discipline, production-kernel ranks only)
+        P = cfg.col_passes
+        w = rank // P if rank % P == 0 else 0
+        self.passes = P if (P > 1 and not self.det and w in _V2_RANKS) else 1
+        self.planes_mode = cfg.col_planes
+        self._planes = {}
+        self._nin = len(plan.shape) - 1
         self.num_tiles = sum(sg["n"] for sg in self.segments)
         self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
         mx = max((sg["n"] for sg in self.segments), default=0)
@@ -376,7 +406,31 @@ class _ShardExec:
 
     @property
     def launches(self) -> int:
-        return sum(1 + len(sg["levels"]) for sg in self.segments)
+        per = sum(1 + len(sg["levels"]) for sg in self.segments)
+        if self.passes == 1:
+            return per
+        return per * self.passes + (self._nin if self.planes_mode else 0)
+
+    def _factor_slices(self, mode, factors, stream):
+        """Per input mode and pass: (pointer, row pitch) of the pass's columns.
+        Planes: one skrp_split_columns launch per input mode per call (the
+        factors change every mode in a chained run)."""
+        P, R = self.passes, self.rank
+        w_ = R // P
+        out = {}
+        for w, f in enumerate(factors):
+            if w == mode:
+                continue
+            if not self.planes_mode:
+                out[w] = [(f.data_ptr() + p * w_ * 4, R) for p in range(P)]
+                continue
+            buf = self._planes.get(w)
+            if buf is None or buf.shape[1] != f.shape[0]:
+                buf = _torch().empty((P, f.shape[0], w_), dtype=torch_float32(), device=f.device)
+                self._planes[w] = buf
+            _lib.call("skrp_split_columns", f.data_ptr(), f.shape[0], R, P, buf.data_ptr(), stream)
+            out[w] = [(buf[p].data_ptr(), w_) for p in range(P)]
+        return out
 
     def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
         """Launch the tile kernel(s) (+ carry trees).  `events` (start, end) CUDA
@@ -402,6 +456,23 @@ class _ShardExec:
         a.flags = self.flags
         if events is not None:
             events[0].record()  # current stream == `stream` (callers launch on it)
+        if self.passes > 1:
+            sl = self._factor_slices(mode, factors, stream)
+            w_ = self.rank // self.passes
+            a.rank = w_
+            a.out_ld = self.rank
+            for p in range(self.passes):
+                for w, lst in sl.items():
+                    a.factors[w] = lst[p][0]
+                    a.factor_ld = lst[p][1]
+                a.out = out.data_ptr() + p * w_ * 4
+                for seg in self.segments:
+                    a.tiles = seg["tiles"].data_ptr()
+                    a.num_tiles = seg["n"]
+                    _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
+            if events is not None:
+                events[1].record()
+            return
         for seg in self.segments:
             a.tiles = seg["tiles"].data_ptr()
             a.num_tiles = seg["n"]
@@ -421,6 +492,130 @@ class _ShardExec:
             events[1].record()
 
 
+class _PanelExec:
+    """Item tables of the output-stationary panel kernel (plan.to_panels) for
+    a set of shards: the items of those shards, in row order.  One launch per
+    mode (per column pass); every owned row is written once, so the output
+    needs no zeroing; the result does not depend on the placement."""
+
+    writes_all_rows = True
+
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+        torch = _torch()
+        pn = plan.panel
+        self.gpu = gpu
+        self.rank = rank
+        self.det = cfg.accumulation == "deterministic-reduce"
+        self.passes = 1
+        mine = np.isin(pn["item_shard"], np.asarray(list(shard_ids), dtype=np.int64))
+        idx = np.nonzero(mine)[0]
+        self.num_items = int(len(idx))
+        self.num_tiles = self.num_items  # "work units" for the runner's accounting
+        self.tile_nnz = 0
+        self.levels = []
+        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.item_rows = torch.from_numpy(np.ascontiguousarray(pn["item_rows"][idx])).to(gpu)
+        ti = torch.from_numpy(idx).to(pn["item_offsets"].device)
+        self.item_offsets = pn["item_offsets"].index_select(0, ti).to(gpu).contiguous()
+        self.groups = pn["groups"]
+        self.warps = pn["warps"]
+        self.slab_rows = 1 << pn["slab_shift"]
+        self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
+        # grid-synchronised rounds only pay when items are about equal
+        # (uniform tensors); skewed items are claimed dynamically
+        sizes = (self.item_offsets[:, -1] - self.item_offsets[:, 0]).double() if self.num_items else None
+        self.lockstep = bool(cfg.panel_lockstep and self.num_items
+                             and float(sizes.max()) <= 1.5 * float(sizes.mean()) + 1.0)
+
+    @property
+    def launches(self) -> int:
+        return 1 if self.num_items else 0
+
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
+        if self.num_items == 0:
+            return
+        a = _lib.MttkrpArgs()
+        a.nmodes = len(coords)
+        a.mode = mode
+        a.rank = self.rank
+        a.accumulation = _lib.ACC_DETERMINISTIC if self.det else _lib.ACC_ATOMIC
+        a.nnz = nnz_total
+        for w, c in enumerate(coords):
+            a.coords[w] = c.data_ptr()
+            a.factors[w] = None if w == mode else factors[w].data_ptr()
+        a.values = vals.data_ptr()
+        a.out = out.data_ptr()
+        a.work_counter = self.counter.data_ptr()
+        a.variant = cfg.kernel_variant
+        pa = _lib.PanelArgs()
+        pa.item_rows = self.item_rows.data_ptr()
+        pa.item_offsets = self.item_offsets.data_ptr()
+        pa.num_items = self.num_items
+        pa.groups = self.groups
+        pa.slab_rows = self.slab_rows
+        pa.warps = self.warps
+        pa.flags = _lib.PANEL_LOCKSTEP if self.lockstep else 0
+        if events is not None:
+            events[0].record()
+        _lib.check(_lib.lib().skrp_mttkrp_panels(ctypes.byref(a), ctypes.byref(pa), stream), "skrp_mttkrp_panels")
+        if events is not None:
+            events[1].record()
+
+
+def panel_shape(nmodes: int, rank: int):
+    """(warps per CTA, largest slab rows) of the panel kernel, or None."""
+    w = ctypes.c_int32()
+    m = ctypes.c_int32()
+    rc = _lib.lib().skrp_panel_shape(nmodes, rank, ctypes.byref(w), ctypes.byref(m))
+    if rc != _lib.SKRP_OK:
+        return None
+    return int(w.value), int(m.value)
+
+
+def choose_panels(plan, rank, cfg: PlatformConfig, shard_ids=None):
+    """Panel layout parameters (slab_shift, input shifts, warps) or None.
+
+    Input blocks: the blocked layout's cost model (choose_blocking with
+    cfg.l2_budget_mb / max_blocks -- the same blocks, measured equally fast on
+    cfg2) unless cfg.panel_l2_mb >= 0, which cuts every input mode whose factor
+    exceeds its share of that budget (tuning / tests).  Slab: the largest power
+    of two whose panel fits cfg.panel_smem_kb of shared memory (the rest of the
+    SM's L1 holds the gathers in flight), capped by the kernel and the mode."""
+    n, d = len(plan.shape), plan.mode
+    shp = panel_shape(n, rank)
+    if shp is None:
+        return None
+    warps, max_slab = shp
+    if cfg.slab_rows:
+        slab = cfg.slab_rows
+    else:
+        slab = warps
+        while slab * 2 * rank * 4 <= cfg.panel_smem_kb * 1024 and slab * 2 <= max_slab:
+            slab *= 2
+    slab = min(slab, max(warps, 1 << max(0, (plan.shape[d] - 1).bit_length())))
+    ins = [w for w in range(n) if w != d]
+    row_b = rank * 4
+    shifts = [-1] * n
+    if cfg.panel_l2_mb < 0:
+        sh, _, _ = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20, max_blocks=cfg.max_blocks, force=True)
+        if sh is not None:
+            shifts = list(sh)
+    else:
+        share = (cfg.panel_l2_mb << 20) / max(1, len(ins))
+        for w in ins:
+            if plan.shape[w] * row_b > share:
+                rows = max(1, int(share // row_b))
+                shift = max(0, rows.bit_length() - 1)
+                while -(-plan.shape[w] // (1 << shift)) > 64:  # bounds the item table
+                    shift += 1
+                shifts[w] = shift
+    return (slab.bit_length() - 1, shifts, warps)
+
+
+def torch_float32():
+    return _torch().float32
+
+
 def _plan_arrays(plan: ModePartitionPlan, gpu):
     """The plan's sorted arrays on `gpu` (copied once and cached if the plan
     was built on another GPU)."""
@@ -434,12 +629,17 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
     return plan._exec_cache[key]
 
 
-def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None) -> _ShardExec:
+def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
     key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout,
-           clip)
+           clip, cfg.col_passes, cfg.col_planes)
     ex = plan._exec_cache.get(key)
     if ex is None:
-        ex = _ShardExec(plan, shard_ids, cfg, rank, gpu, clip)
+        if plan.layout == "panel":
+            if clip is not None:
+                raise ValueError("element-split placement needs the plan-order (flycoo) layout")
+            ex = _PanelExec(plan, shard_ids, cfg, rank, gpu)
+        else:
+            ex = _ShardExec(plan, shard_ids, cfg, rank, gpu, clip)
         plan._exec_cache[key] = ex
     return ex
 

@@ -143,7 +143,9 @@ class ModePartitionPlan:
         # "blocked" (see to_blocked); groups: per shard, [start, stop) ranges
         self.layout = "flycoo"
         self.block_shifts = None
+        self.block_order = None
         self.groups = None
+        self.panel = None
         self.shards = [
             TensorShard(self, mode, j, (int(self.bounds[j]), int(self.bounds[j + 1])),
                         int(self.offsets[j]), int(self.offsets[j + 1]),
@@ -221,26 +223,33 @@ class ModePartitionPlan:
         out[self.exec_perm.cpu().numpy().astype(np.int64)] = arr
         return out
 
-    def to_blocked(self, shifts):
+    def to_blocked(self, shifts, order=None):
         """Reorder the device arrays IN PLACE into the L2-blocked execution
         layout: inside every shard, nonzeros are grouped by the blocks
-        (c_w >> shifts[w]) of the blocked input modes and stay sorted by c_d
-        inside each group (stable sort by [shard | blocks]).  Shard offsets are
-        unchanged; the host-visible plan (``_indices``, ``_values``, ISPs) keeps
-        the reference order (it is derived from the source tensor + order).
-        The per-mode factor rows touched by one group then fit in L2."""
+        (c_w >> shifts[w]) of the blocked modes and stay sorted by c_d inside
+        each group (stable sort by [shard | blocks]).  ``shifts[mode] >= 0``
+        also cuts the OUTPUT rows into blocks, so a run of groups shares one
+        L2-resident output block.  ``order`` = blocked modes by key
+        significance (default: the output mode first, then the input modes
+        ascending): the work queue runs groups in that order, so the last
+        mode's block changes fastest.  Shard offsets are unchanged; the
+        host-visible plan (``_indices``, ``_values``, ISPs) keeps the
+        reference order (it is derived from the source tensor + order)."""
         import torch
 
         if self.layout != "flycoo":
             raise ValueError("plan is already in a blocked layout")
         n = len(self.shape)
         shifts = [int(x) for x in shifts]
-        if len(shifts) != n or shifts[self.mode] >= 0:
-            raise ValueError("need one shift per mode, and none for the output mode")
+        if len(shifts) != n:
+            raise ValueError("need one shift per mode")
         if all(x < 0 for x in shifts):
             return self
-        if self._host_idx is None and self._source is not None and self.perm is not None:
-            pass  # host views stay derivable from source + order
+        if order is None:
+            order = ([self.mode] if shifts[self.mode] >= 0 else []) + [w for w in range(n) if w != self.mode]
+        order = [int(w) for w in order if shifts[int(w)] >= 0]
+        if sorted(order) != [w for w in range(n) if shifts[w] >= 0]:
+            raise ValueError("order must list every blocked mode once")
         widths = [0] * n
         for w in range(n):
             if shifts[w] >= 0:
@@ -250,37 +259,13 @@ class ModePartitionPlan:
         total_bits = shard_bits + sum(widths)
         if total_bits > 32:
             raise ValueError(f"blocked key needs {total_bits} > 32 bits")
-        nnz = self.nnz
+        sorted_keys = self._reorder_by_key([(self.coords[w], shifts[w], widths[w]) for w in order], shard_bits)
         dev = self.vals.device
         stream = torch.cuda.current_stream(dev).cuda_stream
-        starts = torch.from_numpy(np.ascontiguousarray(self.offsets)).to(dev)
-        keys = torch.empty(nnz, dtype=torch.int32, device=dev)
-        cptr = (_lib.vp * n)(*[c.data_ptr() for c in self.coords])
-        sh = np.ascontiguousarray(shifts, dtype=np.int32)
-        wd = np.ascontiguousarray(widths, dtype=np.int32)
-        _lib.call("skrp_block_keys", cptr, n, sh.ctypes.data, wd.ctypes.data, starts.data_ptr(), k, shard_bits,
-                  nnz, keys.data_ptr(), stream)
-        sorted_keys = torch.empty_like(keys)
-        perm = torch.empty_like(keys)
-        ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, total_bits)
-        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
-        _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), nnz, total_bits, sorted_keys.data_ptr(),
-                  perm.data_ptr(), ws.data_ptr(), ws_bytes, stream)
-        del ws, keys
         # group sizes: histogram of the sorted keys (bins = 2^total_bits)
         counts = torch.empty(1 << total_bits, dtype=torch.int64, device=dev)
-        _lib.call("skrp_histogram", sorted_keys.data_ptr(), nnz, 1 << total_bits, counts.data_ptr(), stream)
+        _lib.call("skrp_histogram", sorted_keys.data_ptr(), self.nnz, 1 << total_bits, counts.data_ptr(), stream)
         del sorted_keys
-        for w in range(n):
-            out = torch.empty_like(self.coords[w])
-            _lib.call("skrp_gather_u32", self.coords[w].data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
-            self.coords[w] = out
-        out = torch.empty_like(self.vals)
-        _lib.call("skrp_gather_u32", self.vals.data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
-        self.vals = out
-        # device position i holds plan-order element exec_perm[i] (kept only when
-        # the plan keeps its permutation, i.e. host views are wanted)
-        self.exec_perm = perm if self.perm is not None else None
         c = counts.cpu().numpy()
         per_shard = 1 << (total_bits - shard_bits)
         self.groups = []
@@ -293,6 +278,110 @@ class ModePartitionPlan:
             self.groups.append(np.stack([begins[keep], ends[keep], gkey], axis=1).astype(np.int64))
         self.layout = "blocked"
         self.block_shifts = shifts
+        self.block_order = order
+        self._exec_cache.clear()
+        torch.cuda.current_stream(dev).synchronize()
+        return self
+
+    def _reorder_by_key(self, parts, shard_bits):
+        """Stable-sort the device arrays IN PLACE by [shard | parts...] (parts:
+        (coordinate array, shift, width) in key order); returns the sorted keys.
+        Keeps ``exec_perm`` (device position -> plan position) when the plan
+        keeps its permutation (host views)."""
+        import torch
+
+        nnz = self.nnz
+        dev = self.vals.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        total_bits = shard_bits + sum(p[2] for p in parts)
+        starts = torch.from_numpy(np.ascontiguousarray(self.offsets)).to(dev)
+        keys = torch.empty(nnz, dtype=torch.int32, device=dev)
+        cptr = (_lib.vp * len(parts))(*[p[0].data_ptr() for p in parts])
+        sh = np.ascontiguousarray([p[1] for p in parts], dtype=np.int32)
+        wd = np.ascontiguousarray([p[2] for p in parts], dtype=np.int32)
+        _lib.call("skrp_block_keys", cptr, len(parts), sh.ctypes.data, wd.ctypes.data, starts.data_ptr(),
+                  self.shard_count, shard_bits, nnz, keys.data_ptr(), stream)
+        sorted_keys = torch.empty_like(keys)
+        perm = torch.empty_like(keys)
+        ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, total_bits)
+        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+        _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), nnz, total_bits, sorted_keys.data_ptr(),
+                  perm.data_ptr(), ws.data_ptr(), ws_bytes, stream)
+        del ws, keys
+        for w in range(len(self.shape)):
+            out = torch.empty_like(self.coords[w])
+            _lib.call("skrp_gather_u32", self.coords[w].data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
+            self.coords[w] = out
+        out = torch.empty_like(self.vals)
+        _lib.call("skrp_gather_u32", self.vals.data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
+        self.vals = out
+        # device position i holds plan-order element exec_perm[i] (kept only when
+        # the plan keeps its permutation, i.e. host views are wanted)
+        self.exec_perm = perm if self.perm is not None else None
+        return sorted_keys
+
+    def to_panels(self, slab_shift, shifts, warps, order=None):
+        """Reorder the device arrays IN PLACE into the PANEL execution layout
+        of the output-stationary kernel (csrc/mttkrp_panel.cuh): key =
+        [shard | slab (c_d >> slab_shift) | input blocks (c_w >> shifts[w], in
+        ``order``) | warp stripe ((c_d >> stripe_shift) mod warps)].  Rows stay
+        sorted inside every (slab, group, stripe) range.  Builds the item
+        table: one ITEM per (shard, slab) intersection with its row range and
+        groups*warps+1 element offsets (``self.panel``).  Shard offsets and
+        the host-visible plan are unchanged, as in to_blocked."""
+        import torch
+
+        if self.layout != "flycoo":
+            raise ValueError("plan is already in a reordered layout")
+        n, d = len(self.shape), self.mode
+        shifts = [int(x) for x in shifts]
+        if len(shifts) != n or shifts[d] >= 0:
+            raise ValueError("need one shift per mode (-1 = unblocked), none for the output mode")
+        if warps < 1 or warps & (warps - 1) or (1 << slab_shift) < warps:
+            raise ValueError("warps must be a power of two <= slab rows")
+        if order is None:
+            order = [w for w in range(n) if w != d]
+        order = [int(w) for w in order if w != d and shifts[int(w)] >= 0]
+        stripe_bits = _key_bits(warps)
+        stripe_shift = slab_shift - stripe_bits
+        slab_w = max(1, _key_bits(-(-self.shape[d] // (1 << slab_shift))))
+        in_w = [max(1, _key_bits(-(-self.shape[w] // (1 << shifts[w])))) for w in order]
+        parts = ([(self.coords[d], slab_shift, slab_w)] + [(self.coords[w], shifts[w], b) for w, b in zip(order, in_w)]
+                 + ([(self.coords[d], stripe_shift, stripe_bits)] if stripe_bits else []))
+        k = self.shard_count
+        shard_bits = max(1, _key_bits(k))
+        group_bits = sum(in_w)
+        total_bits = shard_bits + slab_w + group_bits + stripe_bits
+        if total_bits > 31:
+            raise ValueError(f"panel key needs {total_bits} > 31 bits (use larger slabs or blocks)")
+        dev = self.vals.device
+        sorted_keys = self._reorder_by_key(parts, shard_bits)
+        # items: (shard, slab) intersections, in row order
+        rows, bases = [], []
+        for j, sh in enumerate(self.shards):
+            lo, hi = sh.index_range
+            if hi <= lo:
+                continue
+            for s_ in range(lo >> slab_shift, ((hi - 1) >> slab_shift) + 1):
+                rows.append((max(lo, s_ << slab_shift), min(hi, (s_ + 1) << slab_shift)))
+                bases.append(((j << slab_w) | s_) << (group_bits + stripe_bits))
+        groups = 1 << group_bits
+        per = groups * warps
+        base = torch.tensor(bases, dtype=torch.int64, device=dev)
+        q = (base[:, None] + torch.arange(per + 1, dtype=torch.int64, device=dev)[None, :])
+        q[:, per] = base + (1 << (group_bits + stripe_bits))  # end of the item = start of the next slab key
+        offs = torch.searchsorted(sorted_keys, q.to(torch.int32).reshape(-1)).reshape(len(bases), per + 1)
+        del sorted_keys
+        self.panel = {
+            "slab_shift": slab_shift, "warps": warps, "groups": groups, "order": order,
+            "item_rows": np.asarray(rows, dtype=np.int64).reshape(-1, 2),
+            "item_shard": np.asarray([b >> (group_bits + stripe_bits + slab_w) for b in bases], dtype=np.int64),
+            "item_offsets": offs.to(torch.int64).contiguous(),
+        }
+        self.groups = None
+        self.layout = "panel"
+        self.block_shifts = shifts
+        self.block_order = order
         self._exec_cache.clear()
         torch.cuda.current_stream(dev).synchronize()
         return self

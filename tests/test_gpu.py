@@ -420,6 +420,151 @@ def test_blocked_layout_parity(golden, name):
             assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL
 
 
+@pytest.mark.parametrize("order_kind", ["default", "reversed"])
+def test_blocked_output_blocks_parity(golden, order_kind):
+    """Output-mode blocks (3-D L2 tiling: out block x input blocks) with the
+    default and a reversed key order: outputs within tolerance for both
+    disciplines, shard ranges and host plan views unchanged."""
+    t = tensor_from(golden, "u3")
+    fs = factors_from(golden, "u3", 32, t.num_modes)
+    ref = golden("mttkrp.npz")
+    plans = golden("plans.npz")
+    for d in range(t.num_modes):
+        p = sk.build_mode_plan(t, d, sk.PartitionConfig(devices=2))
+        shards_before = [(s_.start, s_.stop, s_.index_range) for s_ in p.shards]
+        shifts = [max(0, (s - 1).bit_length() - 2) for s in t.shape]  # ~4 blocks per mode
+        order = None if order_kind == "default" else list(range(t.num_modes))[::-1]
+        p.to_blocked(shifts, order)
+        assert p.block_order == (order or [d] + [w for w in range(t.num_modes) if w != d])
+        assert [(s_.start, s_.stop, s_.index_range) for s_ in p.shards] == shards_before
+        for s_, g in zip(p.shards, p.groups):
+            if s_.nnz:
+                assert g[0, 0] == s_.start and g[-1, 1] == s_.stop and np.all(g[1:, 0] == g[:-1, 1])
+        assert np.array_equal(p._indices, plans[f"u3_m{d}_sorted_indices"])
+        for acc in ("atomic", "deterministic-reduce"):
+            cfg = sk.PlatformConfig(devices=2, rank=32, accumulation=acc, tile_nnz=32, layout="blocked")
+            out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+            assert rel_err(out, ref[f"u3_R32_oracle_{d}"]) <= TOL
+
+
+@pytest.mark.parametrize("passes,planes,layout", [(2, True, "blocked"), (2, False, "blocked"), (4, True, "flycoo"),
+                                                  (2, True, "flycoo")])
+def test_column_passes_parity(golden, passes, planes, layout):
+    """Column passes (each launch gathers R/passes columns from column planes
+    or strided row slices, writes its column slice of the output): same
+    outputs within tolerance as the oracle, all modes, chained."""
+    t = sk.synth_tensor((300, 200, 150), 200_000, seed=5)
+    fs = sk.random_factors(t.shape, 32, seed=2)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=2, isp_capacity=1024))
+    cfg = sk.PlatformConfig(devices=2, rank=32, accumulation="atomic", tile_nnz=64, layout=layout,
+                            l2_budget_mb=0, col_passes=passes, col_planes=planes)
+    outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(outs[d], expect) <= TOL
+        facs[d] = outs[d]
+
+
+@pytest.mark.parametrize("name", ["u3", "z3", "z4", "u5"])
+def test_panel_layout_parity(golden, name):
+    """Output-stationary panel layout (slabs x block groups x warp stripes):
+    every mode within tolerance of the oracle, shard ranges unchanged, host
+    plan views still bit-exact, item rows tile every shard's row range."""
+    from paper_2507_15121_b200.engine import panel_shape
+
+    t = tensor_from(golden, name)
+    fs = factors_from(golden, name, 32, t.num_modes)
+    ref = golden("mttkrp.npz")
+    plans = golden("plans.npz")
+    warps, _ = panel_shape(t.num_modes, 32)
+    for d in range(t.num_modes):
+        p = sk.build_mode_plan(t, d, sk.PartitionConfig(devices=2))
+        shards_before = [(s_.start, s_.stop, s_.index_range) for s_ in p.shards]
+        shifts = [-1 if w == d else max(0, (s - 1).bit_length() - 2) for w, s in enumerate(t.shape)]
+        p.to_panels(4, shifts, warps)  # 16-row slabs: many items, slabs straddle shards
+        assert p.layout == "panel"
+        assert [(s_.start, s_.stop, s_.index_range) for s_ in p.shards] == shards_before
+        assert np.array_equal(p._indices, plans[f"{name}_m{d}_sorted_indices"])
+        rows = p.panel["item_rows"]
+        for j, s_ in enumerate(p.shards):
+            mine = rows[p.panel["item_shard"] == j]
+            lo, hi = s_.index_range
+            if hi > lo:
+                assert mine[0, 0] == lo and mine[-1, 1] == hi and np.all(mine[1:, 0] == mine[:-1, 1])
+        offs = p.panel["item_offsets"].cpu().numpy()
+        assert np.all(np.diff(offs, axis=1) >= 0)
+        for acc in ("atomic", "deterministic-reduce"):
+            cfg = sk.PlatformConfig(devices=2, rank=32, accumulation=acc)
+            out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+            assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL
+
+
+@pytest.mark.parametrize("rank", [8, 16, 32, 64])
+def test_panel_all_modes_device_invariance(rank):
+    """Panel layout through the engine (layout='panel', tiny L2 budget ->
+    several block groups): chained all-mode parity for R in {8,16,32,64}, and
+    bit-identical outputs for any device count / placement."""
+    t = sk.synth_tensor((700, 300, 260), 300_000, seed=4)
+    fs = sk.random_factors(t.shape, rank, seed=1)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4, isp_capacity=512))
+    results = []
+    for m, sched in [(1, "dynamic"), (2, "static"), (4, "contiguous")]:
+        cfg = sk.PlatformConfig(devices=m, rank=rank, scheduling=sched, layout="panel", panel_l2_mb=0,
+                                slab_rows=64, panel_lockstep=(m != 2))
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        results.append(outs)
+    assert all(p.layout == "panel" and p.panel["groups"] > 1 for p in plans)
+    for outs in results[1:]:
+        for a, b in zip(results[0], outs):
+            assert np.array_equal(a, b)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(results[0][d], expect) <= TOL
+        facs[d] = results[0][d]
+
+
+@pytest.mark.parametrize("variant", [4, 5])
+def test_panel_slot_variants(variant):
+    """Slot-sequential panel ranges (kernel variants 4/5, R=32, N=3): chained
+    all-mode parity and bit-identical results for 1 and 3 devices."""
+    t = sk.synth_tensor((900, 500, 400), 400_000, seed=6)
+    fs = sk.random_factors(t.shape, 32, seed=2)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=3, isp_capacity=512))
+    results = []
+    for m in (1, 3):
+        cfg = sk.PlatformConfig(devices=m, rank=32, scheduling="static", layout="panel", panel_l2_mb=0,
+                                slab_rows=128, kernel_variant=variant)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        results.append(outs)
+    for a_, b_ in zip(*results):
+        assert np.array_equal(a_, b_)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(results[0][d], expect) <= TOL
+        facs[d] = results[0][d]
+
+
+def test_split_columns_kernel():
+    """skrp_split_columns: plane p == columns [p*w, (p+1)*w) of the source."""
+    import torch
+
+    from paper_2507_15121_b200 import _lib
+
+    src = torch.randn(1000, 64, device="cuda")
+    for parts in (1, 2, 4, 8):
+        dst = torch.empty(parts, 1000, 64 // parts, device="cuda")
+        _lib.call("skrp_split_columns", src.data_ptr(), 1000, 64, parts, dst.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        for p in range(parts):
+            assert torch.equal(dst[p], src[:, p * 64 // parts:(p + 1) * 64 // parts])
+    with pytest.raises(ValueError):
+        _lib.call("skrp_split_columns", src.data_ptr(), 1000, 64, 3, dst.data_ptr(), 0)
+
+
 def test_blocked_deterministic_device_count_invariance():
     """Deterministic-reduce in the blocked layout (one launch per block group,
     read-add-write flushes, additive carry trees): bit-identical results for

@@ -40,7 +40,7 @@ def test_library_exports_every_header_symbol():
 def test_library_host_entry_points_without_gpu():
     """Host-only C functions (no device needed): bounds + version + errors."""
     lib = _lib.lib()
-    assert lib.skrp_abi_version() == 1
+    assert lib.skrp_abi_version() == _lib.ABI_VERSION
     b = np.empty(3, dtype=np.int64)
     _lib.call("skrp_equal_index_bounds", 8, 2, b.ctypes.data)
     assert b.tolist() == [0, 4, 8]

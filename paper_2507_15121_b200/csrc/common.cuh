@@ -121,6 +121,13 @@ __device__ __forceinline__ void ld_row8_na(float (&v)[8], const float *p, uint64
         : "l"(p), "l"(pol));
 }
 
+// L2 prefetch of one 128-B line (no register, no L1 allocation): issued a
+// batch ahead of the gather that will read it
+__device__ __forceinline__ void prefetch_l2_last(const void *p)
+{
+    asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
+}
+
 // no eviction hint (A/B of the L2 policy)
 __device__ __forceinline__ void ld_row8_plain(float (&v)[8], const float *p)
 {

@@ -345,11 +345,11 @@ static Variant mk()
     return v;
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0>
 static Variant mk2()
 {
     Variant v;
-    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL>;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL, PF>;
     v.smem = v2_smem_bytes<8 * LPN>();
     return v;
 }
@@ -430,6 +430,9 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 11 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 0>();  // output: no hint
         if (a.variant == 12 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1, 0>();  // no factor/output hints
         if (a.variant == 13 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 0>();  // 24 warps/SM, output normal
+        // L2 prefetch of the next batch's rows (A/B)
+        if (a.variant == 17 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 1, 1>();
+        if (a.variant == 18 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 1, 1>();
         // column-pass (R = 16 per pass) A/B variants
         if (a.variant == 14 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 2>();
         if (a.variant == 15 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 3, 0, 0>();
@@ -464,10 +467,10 @@ struct PanelVariant {
     size_t stage = 0;
 };
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0>
 static PanelVariant mkp()
 {
-    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG>, NW, 8 * LPN, panel_stage_bytes<8 * LPN, NW>()};
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF>, NW, 8 * LPN, panel_stage_bytes<8 * LPN, NW>()};
 }
 
 static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
@@ -481,6 +484,7 @@ static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
     if (nmodes == 3 && rank == 32 && variant == 4) return mkp<3, 4, 4, 16, 0, 1>();
     if (nmodes == 3 && rank == 32 && variant == 5) return mkp<3, 4, 2, 16, 0, 1>();
     if (nmodes == 3 && rank == 32 && variant == 6) return mkp<3, 4, 8, 16, 0, 1>();
+    if (nmodes == 3 && rank == 32 && variant == 7) return mkp<3, 4, 4, 16, 0, 0, 1>();  // L2 prefetch
     if (nmodes == 3) {
         switch (rank) {
         case 8: return mkp<3, 1, 1, 16>();

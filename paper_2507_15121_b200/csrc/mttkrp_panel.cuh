@@ -47,7 +47,7 @@ __device__ __forceinline__ void grid_wait(unsigned long long *counter, unsigned 
     }
 }
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0>
 __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     mttkrp_panel_kernel(const skrp_mttkrp_args a, const skrp_panel_args pa)
 {
@@ -274,16 +274,43 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             };
             uint32_t nr_l, nc_l[NIN];
             float nv_l;
-            auto fetch = [&](int64_t nbase) {
+            // PF: metadata two batches ahead; the rows of batch i+1 are prefetched
+            // into L2 while batch i gathers (no registers held by the prefetches)
+            uint32_t fr_l = 0, fc_l[NIN];
+            float fv_l = 0.f;
+            auto fetch_to = [&](int64_t nbase, uint32_t &r, float &vv_, uint32_t (&c)[NIN]) {
                 const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
                 const bool v = lane < nn;
                 const int64_t src = nbase + (v ? lane : nn - 1);
-                nr_l = ld_stream_u32(rowc + src, pol_stream);
-                nv_l = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
+                r = ld_stream_u32(rowc + src, pol_stream);
+                vv_ = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
 #pragma unroll
-                for (int j = 0; j < NIN; ++j) nc_l[j] = ld_stream_u32(C[j] + src, pol_stream);
+                for (int j = 0; j < NIN; ++j) c[j] = ld_stream_u32(C[j] + src, pol_stream);
+            };
+            auto fetch = [&](int64_t nbase) { fetch_to(nbase, nr_l, nv_l, nc_l); };
+            // advance the metadata pipeline at the start of the batch at `base`
+            auto advance = [&](int64_t base) {
+                if constexpr (PF) {
+                    if (base + 32 < b1) {
+                        nr_l = fr_l;
+                        nv_l = fv_l;
+#pragma unroll
+                        for (int j = 0; j < NIN; ++j) {
+                            nc_l[j] = fc_l[j];
+                            const float *rowp = F[j] + (size_t)fc_l[j] * fld;
+#pragma unroll
+                            for (int k = 0; k < (RR * 4 + 127) / 128; ++k) prefetch_l2_last(rowp + 32 * k);
+                        }
+                        if (base + 64 < b1) fetch_to(base + 64, fr_l, fv_l, fc_l);
+                    }
+                } else {
+                    if (base + 32 < b1) fetch(base + 32);
+                }
             };
             fetch(b0);
+            if constexpr (PF) {
+                if (b0 + 32 < b1) fetch_to(b0 + 32, fr_l, fv_l, fc_l);
+            }
             uint32_t cur = __shfl_sync(kFull, nr_l, 0);
             for (int64_t base = b0; base < b1; base += 32) {
                 const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
@@ -292,7 +319,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                 uint32_t c_l[NIN];
 #pragma unroll
                 for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
-                if (base + 32 < b1) fetch(base + 32);
+                advance(base);
                 const bool uniform = __all_sync(kFull, r_l == cur);
                 int cls = 0, e_b = 32;
                 unsigned cm = 0;

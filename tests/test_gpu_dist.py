@@ -73,9 +73,10 @@ def _worker(rank, world, port, q):
                     assert torch.equal(lp.vals[la:lb], rp.vals[a:b])
             fs = sk.random_factors(shape, 16, seed=1)
             dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
-            for acc, layout in [("deterministic-reduce", "flycoo"), ("atomic", "blocked")]:
+            for acc, layout in [("deterministic-reduce", "flycoo"), ("atomic", "blocked"),
+                                ("deterministic-reduce", "panel")]:
                 cfg = sk.PlatformConfig(devices=world, rank=16, accumulation=acc, layout=layout, l2_budget_mb=0,
-                                        tile_nnz=64)
+                                        tile_nnz=64, panel_l2_mb=0, slab_rows=64)
                 lplans = [build_mode_plan_distributed(chunk, d, pcfg) for d in range(len(shape))]
                 runner = DistributedMttkrp(lplans, cfg)
                 outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]

@@ -91,3 +91,14 @@ def test_plan_and_mttkrp_properties(c):
                 out, _ = sk.mttkrp_mode(q, sk.make_devices(fs, cfg), cfg, update_factors=False)
             err = np.max(np.abs(out - expect) / np.maximum(np.abs(expect), 1.0))
             assert err <= 1e-4, ("blocked", d, err)
+            # output-stationary panel layout (small slabs, several block groups)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                q = sk.build_mode_plan(t, d, pcfg)
+            cfg = sk.PlatformConfig(devices=c["devices"], rank=c["rank"], layout="panel", panel_l2_mb=0,
+                                    slab_rows=64)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                out, _ = sk.mttkrp_mode(q, sk.make_devices(fs, cfg), cfg, update_factors=False)
+            err = np.max(np.abs(out - expect) / np.maximum(np.abs(expect), 1.0))
+            assert err <= 1e-4, ("panel", d, err)

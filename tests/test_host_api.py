@@ -246,3 +246,28 @@ def test_elementwise_compute_spec():
     row, contrib = sk.elementwise_compute(sk.NonzeroElement((0, 1, 2), 2.0), [a, b, np.zeros((3, 2))], 2)
     assert row == 2 and contrib.tolist() == [6.0, 16.0]
     assert sk.khatri_rao([[1.0], [2.0]], [[3.0], [4.0]]).ravel().tolist() == [3.0, 4.0, 6.0, 8.0]
+
+
+def test_choose_panels_key_budget():
+    """Panel layout parameters (host logic, no GPU): the slab fits the shared
+    memory budget, blocks respect the key budget of to_panels (<= 30 bits,
+    <= 2^12 group slots) for 3..5 modes and tiny L2 budgets."""
+    from types import SimpleNamespace
+
+    from paper_2507_15121_b200.engine import PlatformConfig, choose_panels, panel_shape
+
+    for shape in [(4_800_000, 1_800_000, 1_800_000), (10_000_000, 1_000_000, 100_000, 1_000),
+                  (5000, 4000, 3000, 2000, 1000), (46, 240_000, 240_000)]:
+        for rank in (8, 16, 32, 64):
+            for d in range(len(shape)):
+                plan = SimpleNamespace(shape=shape, mode=d, shard_count=32)
+                cfg = PlatformConfig(rank=rank, layout="panel", panel_l2_mb=0)
+                slab_shift, shifts, warps = choose_panels(plan, rank, cfg)
+                assert warps == panel_shape(len(shape), rank)[0]
+                slab = 1 << slab_shift
+                assert slab * rank * 4 <= cfg.panel_smem_kb * 1024 or slab == warps
+                assert shifts[d] == -1
+                gb = sum(max(1, (-(-shape[w] // (1 << shifts[w])) - 1).bit_length())
+                         for w in range(len(shape)) if w != d and shifts[w] >= 0)
+                total = 5 + max(1, (-(-shape[d] // slab) - 1).bit_length()) + gb + (warps.bit_length() - 1)
+                assert gb <= 12 and total <= 30, (shape, rank, d, shifts)

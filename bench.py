@@ -84,6 +84,23 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def pcie_h2d_gbs(dev, nbytes=1 << 31):
+    """Measured pinned host -> device copy bandwidth (the out-of-core bound)."""
+    import torch
+
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
+
+
 def lookup_traffic(config, kernel):
     """DRAM read+write bytes per launch of `kernel` on `config` from one ncu
     --set full capture (profiles/ncu_traffic.json), or None."""
@@ -310,6 +327,14 @@ def run_ours(args, cfg):
     if args.shifts:
         for p_, sh in zip(plans, args.shifts.split(";")):
             p_.to_blocked([int(x) for x in sh.split(",")])
+    streamed = []
+    if args.stream_modes:
+        # out-of-core execution: these modes' plans live
+        # in pinned host memory and are streamed to HBM chunk by chunk each step
+        streamed = list(range(len(plans))) if args.stream_modes == "all" else [int(x) for x in args.stream_modes.split(",")]
+        for i in streamed:
+            plans[i].to_host()
+        torch.cuda.empty_cache()
     runner = DistributedMttkrp(plans, pl, rank=rank, world=world, device=dev)
     runner.prepare(R)
     setup_s = time.perf_counter() - t_setup
@@ -332,7 +357,7 @@ def run_ours(args, cfg):
     clocks.start()
     time.sleep(0.3)
     graph = None
-    if world == 1 and not args.no_graph:
+    if world == 1 and not args.no_graph and not streamed:
         graph = runner.capture(dev_f)  # whole all-mode step as one CUDA graph
         graph.replay()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -383,6 +408,7 @@ def run_ours(args, cfg):
     x1 = torch.cuda.Event(enable_timing=True)
     x0.record()
     h2d, d2h = runner.run_host_pipelined(host_f, host_out, args.steps)
+    h2d += sum(runner._exec(i, R).h2d_bytes for i in streamed)  # streamed plans cross the link every step
     x1.record()
     barrier()
     e2e_s = x0.elapsed_time(x1) / 1e3 / args.steps
@@ -391,9 +417,18 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    stream_info = None
+    if streamed:
+        ex_bytes = sum(runner._exec(i, R).h2d_bytes for i in streamed)
+        stream_info = {"modes": streamed, "h2d_plan_bytes_per_step": ex_bytes,
+                       "streamed_modes_ms": [kern[i] * 1e3 for i in streamed],
+                       "h2d_plan_gbs": ex_bytes / sum(kern[i] for i in streamed) / 1e9,
+                       "pcie_h2d_copy_gbs": pcie_h2d_gbs(dev),
+                       "chunk_nnz": pl.stream_chunk_nnz}
+
     # ---- parity on a seeded sample of output rows (chained replay, fp64)
     parity = None
-    if rank == 0 and not args.no_parity:
+    if rank == 0 and not args.no_parity and not streamed:
         parity = sample_parity(plans, init, runner.outputs, modes, rows_per_mode=args.parity_rows,
                                owned=[runner.ownership[i][rank] for i in range(len(modes))] if dist_build else None)
 
@@ -430,6 +465,7 @@ def run_ours(args, cfg):
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": launches,
+            "stream": stream_info,
             "clocks": clk,
             "cpu_baseline": cpu,
             "parity": parity,
@@ -613,6 +649,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
+    ap.add_argument("--stream-modes", default="", help="out-of-core: stream these modes' plans from pinned host "
+                                                      "memory ('all' or e.g. '0,2'; atomic accumulation)")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     args = ap.parse_args()

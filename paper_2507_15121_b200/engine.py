@@ -72,6 +72,7 @@ class PlatformConfig:
     slab_rows: int = 0          # panel layout: output rows per slab (0 = auto, see panel_smem_kb)
     panel_smem_kb: int = 64     # panel layout: shared memory for the output panel (auto slab size)
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
+    stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -493,6 +494,104 @@ class _ShardExec:
             events[1].record()
 
 
+class _StreamExec:
+    """Out-of-core executor: the plan lives in pinned
+    host memory (plan.to_host()); each run copies it to two device buffers
+    chunk by chunk on a copy stream while the tile kernel processes the
+    previous chunk (double buffering, events both ways).  A chunk is a
+    contiguous element range of whole tiles; rows may straddle chunks, so
+    every flush adds (atomic discipline).  HBM holds only 2 chunks + the
+    factors + the output, whatever the tensor size; the rate is bound by the
+    host->device link (PCIe), not HBM."""
+
+    writes_all_rows = False
+
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+        torch = _torch()
+        if cfg.accumulation != "atomic":
+            raise ValueError("out-of-core (streamed) plans run under accumulation='atomic' (rows straddle chunks)")
+        self.gpu = gpu
+        self.rank = rank
+        self.det = False
+        self.passes = 1
+        self.levels = []
+        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
+        tiles, _ = tile_table(plan, shard_ids, self.tile_nnz)
+        s_, e_ = tiles[0::2], tiles[1::2]
+        cap = max(int(cfg.stream_chunk_nnz), self.tile_nnz)
+        self.chunks = []  # (elem start, elem end, device tile table (chunk-local))
+        i, n = 0, len(s_)
+        while i < n:
+            j = i + 1
+            while j < n and s_[j] == e_[j - 1] and e_[j] - s_[i] <= cap:
+                j += 1
+            c0, c1 = int(s_[i]), int(e_[j - 1])
+            t = np.empty(2 * (j - i), dtype=np.int64)
+            t[0::2] = s_[i:j] - c0
+            t[1::2] = e_[i:j] - c0
+            self.chunks.append((c0, c1, torch.from_numpy(t).to(gpu)))
+            i = j
+        self.num_tiles = n
+        self.h2d_bytes = sum(c1 - c0 for c0, c1, _ in self.chunks) * 4 * (len(plan.shape) + 1)
+        big = max((c1 - c0 for c0, c1, _ in self.chunks), default=0)
+        nmodes = len(plan.shape)
+        self.bufs = [([torch.empty(big, dtype=torch.int32, device=gpu) for _ in range(nmodes)],
+                      torch.empty(big, dtype=torch.float32, device=gpu)) for _ in range(2 if len(self.chunks) > 1 else 1)]
+        self.copy_stream = torch.cuda.Stream(gpu)
+        self.ready = [torch.cuda.Event() for _ in self.bufs]
+        self.free = [torch.cuda.Event() for _ in self.bufs]
+        self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
+
+    @property
+    def launches(self) -> int:
+        return len(self.chunks)
+
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
+        torch = _torch()
+        if not self.chunks:
+            return
+        cur = torch.cuda.current_stream(self.gpu)
+        cs = self.copy_stream
+        a = _lib.MttkrpArgs()
+        a.nmodes = len(coords)
+        a.mode = mode
+        a.rank = self.rank
+        a.accumulation = _lib.ACC_ATOMIC
+        for w in range(len(coords)):
+            a.factors[w] = None if w == mode else factors[w].data_ptr()
+        a.out = out.data_ptr()
+        a.work_counter = self.counter.data_ptr()
+        a.variant = cfg.kernel_variant
+        a.flags = _lib.FLAG_ADDITIVE
+        if events is not None:
+            events[0].record()
+        cs.wait_stream(cur)  # buffers may still be read by the previous run
+        nb = len(self.bufs)
+        for i, (c0, c1, tiles) in enumerate(self.chunks):
+            b = i % nb
+            bc, bv = self.bufs[b]
+            n = c1 - c0
+            if i >= nb:
+                cs.wait_event(self.free[b])
+            with torch.cuda.stream(cs):
+                for w in range(len(coords)):
+                    bc[w][:n].copy_(coords[w][c0:c1], non_blocking=True)
+                bv[:n].copy_(vals[c0:c1], non_blocking=True)
+                self.ready[b].record(cs)
+            cur.wait_event(self.ready[b])
+            for w in range(len(coords)):
+                a.coords[w] = bc[w].data_ptr()
+            a.values = bv.data_ptr()
+            a.nnz = n
+            a.tiles = tiles.data_ptr()
+            a.num_tiles = tiles.numel() // 2
+            _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), cur.cuda_stream), "skrp_mttkrp_tiles")
+            self.free[b].record(cur)
+        if events is not None:
+            events[1].record()
+
+
 class _PanelExec:
     """Item tables of the output-stationary panel kernel (plan.to_panels) for
     a set of shards: the items of those shards, in row order.  One launch per
@@ -637,9 +736,12 @@ def torch_float32():
 
 def _plan_arrays(plan: ModePartitionPlan, gpu):
     """The plan's sorted arrays on `gpu` (copied once and cached if the plan
-    was built on another GPU)."""
+    was built on another GPU); host-resident (out-of-core) plans are returned
+    as they are -- their executor streams them."""
     if plan.vals is None:
         raise ValueError("plan has no device arrays (released)")
+    if plan.layout == "host":
+        return plan.coords, plan.vals
     if plan.vals.device == gpu:
         return plan.coords, plan.vals
     key = ("arrays", str(gpu))
@@ -657,6 +759,10 @@ def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
             if clip is not None:
                 raise ValueError("element-split placement needs the plan-order (flycoo) layout")
             ex = _PanelExec(plan, shard_ids, cfg, rank, gpu)
+        elif plan.layout == "host":
+            if clip is not None:
+                raise ValueError("element-split placement is not streamed")
+            ex = _StreamExec(plan, shard_ids, cfg, rank, gpu)
         else:
             ex = _ShardExec(plan, shard_ids, cfg, rank, gpu, clip)
         plan._exec_cache[key] = ex

@@ -215,7 +215,7 @@ class ModePartitionPlan:
         return self._host_vals
 
     def _to_plan_order(self, arr):
-        if self.layout == "flycoo":
+        if self.layout in ("flycoo", "host"):
             return arr
         if getattr(self, "exec_perm", None) is None:
             raise ValueError("blocked plan built without its permutation: host views unavailable")
@@ -384,6 +384,30 @@ class ModePartitionPlan:
         self.block_order = order
         self._exec_cache.clear()
         torch.cuda.current_stream(dev).synchronize()
+        return self
+
+    def to_host(self):
+        """Out-of-core execution (the B200 form of the
+        reference's per-mode staging, engine.py:103-105): move the sorted
+        arrays to PINNED host memory and free their HBM; the stream executor
+        (engine._StreamExec) copies them back chunk by chunk, overlapped with
+        the kernel, every time the mode runs.  Plan order only."""
+        import torch
+
+        if self.layout != "flycoo":
+            raise ValueError("out-of-core execution streams the plan (FLYCOO) order")
+
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        self.coords = [pin(c) for c in self.coords]
+        self.vals = pin(self.vals)
+        if self.perm is not None:
+            self.perm = self.perm.cpu()
+        self.layout = "host"
+        self._exec_cache.clear()
         return self
 
     def release_device(self):

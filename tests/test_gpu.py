@@ -717,3 +717,41 @@ def test_runner_pipelined_host_path(golden):
     for b in range(2):
         for got, want in zip(host_o[b], eager):
             assert rel_err(got.double().numpy(), want.double().cpu().numpy()) <= 1e-6
+
+
+# ----------------------------------------------------------- out-of-core plans
+
+
+@pytest.mark.parametrize("m", [1, 2])
+def test_out_of_core_streamed_modes(m):
+    """Plans moved to pinned host memory are streamed
+    chunk by chunk through two device buffers: chained all-mode parity with
+    modes 0 and 2 out of core (many chunks, rows straddling chunks), host
+    plan views unchanged, HBM freed."""
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    t = sk.synth_tensor((500, 400, 300), 300_000, seed=9)
+    fs = sk.random_factors(t.shape, 32, seed=4)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=m, isp_capacity=1024))
+    before = [p._indices.copy() for p in plans]
+    for d in (0, 2):
+        plans[d].to_host()
+        assert plans[d].layout == "host" and plans[d].vals.is_pinned() and not plans[d].coords[0].is_cuda
+    cfg = sk.PlatformConfig(devices=m, rank=32, accumulation="atomic", stream_chunk_nnz=20_000, tile_nnz=256)
+    outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(outs[d], expect) <= TOL
+        facs[d] = outs[d]
+        assert np.array_equal(plans[d]._indices, before[d])
+    # the one-process-per-GPU runner streams the same plans
+    runner = DistributedMttkrp(plans, sk.PlatformConfig(rank=32, accumulation="atomic", stream_chunk_nnz=50_000),
+                               rank=0, world=1)
+    dev_f = [torch.from_numpy(f.data.astype(np.float32)).cuda() for f in fs]
+    got = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+    for d in range(3):
+        assert rel_err(got[d], outs[d]) <= TOL
+    with pytest.raises(ValueError, match="atomic"):
+        cfgd = sk.PlatformConfig(devices=m, rank=32, accumulation="deterministic-reduce")
+        sk.mttkrp_mode(plans[0], sk.make_devices(fs, cfgd), cfgd)

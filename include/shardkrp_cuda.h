@@ -170,6 +170,27 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
  * rank); 0 on success, SKRP_ERR_INVALID when no panel kernel exists. */
 int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows);
 
+/* ------------------------------------------------ .tns ingestion (§8(f) 4)
+ * GPU restatement of parse_tns (reference tensor.py:173-247).  text: the file
+ * bytes in device memory.  Lines: chunked newline counts -> exclusive scan ->
+ * starts[0] = 0, starts[1 + k] = position after the k-th newline; a final
+ * line without '\n' counts.  classify: kind 0 blank / 1 '#' comment / 2
+ * data, ntok = whitespace-separated tokens.  parse (data lines): nmodes
+ * integer tokens then one float token, exact round-to-nearest-even binary64
+ * (Clinger fast path / Eisel-Lemire); flags[line] bit k (bit 31 = value) marks
+ * a token outside the fast grammar that the caller must parse itself. */
+int skrp_tns_count_lines(const uint8_t *text, int64_t n, int64_t chunk, int64_t *counts, skrp_stream_t stream);
+int skrp_tns_line_starts(const uint8_t *text, int64_t n, int64_t chunk, const int64_t *chunk_offsets, int64_t *starts,
+                         skrp_stream_t stream);
+int skrp_tns_classify(const uint8_t *text, int64_t n, const int64_t *starts, int64_t n_newlines, int64_t nlines,
+                      int8_t *kind, int32_t *ntok, skrp_stream_t stream);
+int skrp_tns_parse(const uint8_t *text, int64_t n, const int64_t *starts, int64_t n_newlines, int64_t nlines,
+                   const int8_t *kind, int32_t nmodes, int64_t *idx, double *vals, uint32_t *flags,
+                   skrp_stream_t stream);
+/* The same token parser on the host (tests): 0 = parsed, 1 = outside the fast
+ * grammar (the caller parses it). */
+int skrp_tns_parse_token_host(const char *tok, int64_t len, int32_t as_int, int64_t *ival, double *dval);
+
 /* Column planes for column-pass execution (B200 addition, no reference
  * counterpart): dst (parts x rows x rank/parts, fp32) plane p = columns
  * [p*rank/parts, (p+1)*rank/parts) of src (rows x rank, row-major).  A pass

@@ -74,6 +74,11 @@ SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
     "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
+    "skrp_tns_count_lines": (i32, [vp, i64, i64, vp, vp]),
+    "skrp_tns_line_starts": (i32, [vp, i64, i64, vp, vp, vp]),
+    "skrp_tns_classify": (i32, [vp, i64, vp, i64, i64, vp, vp, vp]),
+    "skrp_tns_parse": (i32, [vp, i64, vp, i64, i64, vp, i32, vp, vp, vp, vp]),
+    "skrp_tns_parse_token_host": (i32, [ctypes.c_char_p, i64, i32, vp, vp]),
     "skrp_set_l2_persisting": (i32, [i64, vp]),
     "skrp_mttkrp_panels": (i32, [vp, vp, vp]),
     "skrp_panel_shape": (i32, [i32, i32, vp, vp]),

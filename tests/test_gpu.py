@@ -755,3 +755,52 @@ def test_out_of_core_streamed_modes(m):
     with pytest.raises(ValueError, match="atomic"):
         cfgd = sk.PlatformConfig(devices=m, rank=32, accumulation="deterministic-reduce")
         sk.mttkrp_mode(plans[0], sk.make_devices(fs, cfgd), cfgd)
+
+
+# ------------------------------------------------------------- .tns on the GPU
+
+
+def test_tns_gpu_golden_cases():
+    """GPU .tns parser against the REFERENCE parser's outputs and exception
+    messages (tests/golden/tns_cases.json): indices, values (bit-exact),
+    shape, LoadStats, errors."""
+    import json
+    import os
+
+    from test_host_api import _tns_check
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "tns_cases.json")) as fh:
+        cases = json.load(fh)
+    for c in cases:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            _tns_check(sk.parse_tns_gpu, c)
+
+
+def test_tns_gpu_large_random_file(tmp_path):
+    """A 300K-line file (comments, blank lines, CRLF, tabs, %.17g / repr
+    values) parsed on the GPU == the host parser; the device arrays are kept
+    and feed the plan build directly."""
+    rng = np.random.default_rng(5)
+    n = 300_000
+    idx = np.stack([rng.integers(1, s + 1, n) for s in (5000, 3000, 2000)], 1)
+    idx = np.unique(idx, axis=0)
+    rng.shuffle(idx)
+    vals = rng.standard_normal(len(idx)) * 10.0 ** rng.integers(-5, 5, len(idx))
+    lines = ["# big", "# shape: 5000 3000 2000"]
+    for k, (r, v) in enumerate(zip(idx, vals)):
+        sep = "\t" if k % 7 == 0 else " "
+        lines.append(sep.join(map(str, r)) + sep + (f"{v:.17g}" if k % 2 else repr(float(v))))
+        if k % 1000 == 0:
+            lines.append("")
+    path = tmp_path / "big.tns"
+    path.write_bytes(("\r\n".join(lines) + "\r\n").encode())
+    t_gpu = sk.parse_tns_gpu(str(path))
+    t_cpu = sk.parse_tns(str(path))
+    assert t_gpu.shape == t_cpu.shape == (5000, 3000, 2000)
+    assert np.array_equal(t_gpu.indices, t_cpu.indices)
+    assert t_gpu.values.tobytes() == t_cpu.values.tobytes()
+    assert t_gpu._dev is not None
+    p = sk.build_mode_plan(t_gpu, 0, sk.PartitionConfig())
+    q = sk.build_mode_plan(t_cpu, 0, sk.PartitionConfig())
+    assert np.array_equal(p.order(), q.order())

@@ -7,6 +7,7 @@ import io
 import os
 import re
 import subprocess
+import warnings
 
 import numpy as np
 import pytest
@@ -271,3 +272,80 @@ def test_choose_panels_key_budget():
                          for w in range(len(shape)) if w != d and shifts[w] >= 0)
                 total = 5 + max(1, (-(-shape[d] // slab) - 1).bit_length()) + gb + (warps.bit_length() - 1)
                 assert gb <= 12 and total <= 30, (shape, rank, d, shifts)
+
+
+def _tns_check(parse, case):
+    import io
+    import json  # noqa: F401
+
+    kw = dict(coalesce_duplicates=case.get("coalesce", False))
+    if case.get("shape"):
+        kw["shape"] = tuple(case["shape"])
+    if case.get("dtype"):
+        kw["value_dtype"] = np.dtype(case["dtype"])
+    if "error" in case:
+        with pytest.raises(Exception) as ei:
+            parse(io.StringIO(case["text"]), **kw)
+        assert type(ei.value).__name__ == case["error"]["type"], (case["name"], ei.value)
+        assert str(ei.value) == case["error"]["message"], case["name"]
+        return
+    t = parse(io.StringIO(case["text"]), **kw)
+    r = case["result"]
+    assert list(t.shape) == r["shape"], case["name"]
+    assert np.array_equal(t.indices.astype(np.int64), np.array(r["indices"], dtype=np.int64).reshape(t.indices.shape))
+    assert str(t.values.dtype) == r["dtype"]
+    got = [float(v).hex() for v in t.values.astype(np.float64)]
+    assert got == r["values"], case["name"]
+    assert dict(nnz=t.stats.nnz, zero_values=t.stats.zero_values, duplicates=t.stats.duplicates,
+                coalesced=t.stats.coalesced) == r["stats"], case["name"]
+
+
+def test_tns_golden_cases_host():
+    """The host .tns parser against the REFERENCE parser's own outputs and
+    error messages (tests/golden/make_tns_golden.py)."""
+    import json
+
+    with open(os.path.join(ROOT, "tests", "golden", "tns_cases.json")) as fh:
+        cases = json.load(fh)
+    for c in cases:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            _tns_check(sk.parse_tns, c)
+
+
+def test_gpu_float_parser_matches_python_float():
+    """The GPU .tns float parser (compiled for the host too): exact binary64,
+    bit-identical to Python's float() on random %.17g / repr / long decimal
+    strings; tokens it cannot decide are flagged, never guessed."""
+    import ctypes
+    import random
+    import struct
+
+    L = _lib.lib()
+    iv, dv = ctypes.c_int64(), ctypes.c_double()
+    rng = random.Random(3)
+    flagged = 0
+    for i in range(60_000):
+        k = i % 4
+        if k == 0:
+            x = struct.unpack("<d", struct.pack("<Q", rng.getrandbits(64)))[0]
+            if x != x or x in (float("inf"), float("-inf")):
+                continue
+            s = f"{x:.17g}"
+        elif k == 1:
+            s = repr(rng.random() * 10.0 ** rng.randint(-30, 30))
+        elif k == 2:
+            s = f"{rng.randint(0, 10 ** rng.randint(1, 25))}e{rng.randint(-340, 310)}"
+        else:
+            s = "0." + "".join(rng.choice("0123456789") for _ in range(rng.randint(1, 30))) + f"e{rng.randint(-320, 300)}"
+        b = s.encode()
+        if L.skrp_tns_parse_token_host(b, len(b), 0, ctypes.byref(iv), ctypes.byref(dv)):
+            flagged += 1
+            continue
+        assert struct.pack("<d", dv.value) == struct.pack("<d", float(s)), s
+    assert flagged < 100
+    for tok, ok in [("12", 0), ("-7", 0), ("+3", 0), ("1_0", 1), ("x", 1), ("1234567890123456789", 1)]:
+        b = tok.encode()
+        assert L.skrp_tns_parse_token_host(b, len(b), 1, ctypes.byref(iv), ctypes.byref(dv)) == ok
+        if not ok:
+            assert iv.value == int(tok)

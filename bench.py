@@ -296,8 +296,9 @@ def run_ours(args, cfg):
     pcfg = sk.PartitionConfig(devices=world, strategy=cfg["strategy"])
     pl = sk.PlatformConfig(devices=world, rank=R, accumulation=args.accumulation, tile_nnz=args.tile,
                            scheduling=args.scheduling,
-                           kernel_variant=args.variant, layout=args.layout, l2_budget_mb=args.l2_mb,
-                           max_blocks=args.max_blocks)
+                           kernel_variant=args.variant,
+                           layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
+                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather)
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
@@ -456,6 +457,10 @@ def run_ours(args, cfg):
                        "layout": [p.layout for p in plans],
                        "block_shifts": [p.block_shifts for p in plans],
                        "parallelism": f"output-row shards x{world}", "scheduling": args.scheduling,
+                       "allgather": ("none (1 GPU)" if world == 1 else
+                                     "fused: panel write-back P2P-stores rows into every rank (CUDA IPC)"
+                                     if any(runner._fused(i) for i in range(len(modes))) else
+                                     "NCCL broadcasts of owned row ranges"),
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -651,6 +656,8 @@ def main():
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
     ap.add_argument("--stream-modes", default="", help="out-of-core: stream these modes' plans from pinned host "
                                                       "memory ('all' or e.g. '0,2'; atomic accumulation)")
+    ap.add_argument("--fused-allgather", action="store_true",
+                    help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     args = ap.parse_args()

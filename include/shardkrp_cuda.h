@@ -68,12 +68,18 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 3: skrp_mttkrp_args.factor_ld / out_ld, panel entry points */
+int skrp_abi_version(void);  /* 4: panel peer-output push, IPC entry points */
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200
  * addition; 0 restores the default).  *granted = the limit now in force. */
 int skrp_set_l2_persisting(int64_t bytes, int64_t *granted);
+/* CUDA IPC for the fused all-gather: handle (64 bytes) + offset of a device
+ * pointer inside its allocation; open on another process (peer access enabled
+ * lazily) -> the pointer there and the mapping base to close later. */
+int skrp_ipc_get_handle(const void *dev_ptr, uint8_t *handle64, int64_t *offset);
+int skrp_ipc_open_handle(const uint8_t *handle64, int64_t offset, void **dev_ptr, void **base_out);
+int skrp_ipc_close_handle(void *base);
 
 /* ------------------------------------------------------ partition (K2/K3) */
 int skrp_histogram(const uint32_t *keys, int64_t n, int64_t num_bins, int64_t *counts,
@@ -158,6 +164,12 @@ typedef struct {
     int32_t slab_rows;            /* rows per slab, power of two                     */
     int32_t warps;                /* warps per CTA == row stripes per slab           */
     int32_t flags;                /* SKRP_PANEL_* bits                               */
+    const uint64_t *peer_out;     /* device array of num_peers output pointers (other
+                                     ranks' buffers, CUDA IPC): every finished row is
+                                     also stored there -- the all-gather fused into
+                                     the write-back (NVLink P2P stores)              */
+    int32_t num_peers;
+    int32_t reserved;
 } skrp_panel_args;
 /* skrp_panel_args.flags: run items in ROUNDS of one item per CTA separated by a
  * grid barrier (cooperative launch), so all CTAs walk the block groups in step

@@ -30,7 +30,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 3  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 4  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -66,6 +66,9 @@ class PanelArgs(ctypes.Structure):
         ("slab_rows", i32),
         ("warps", i32),
         ("flags", i32),
+        ("peer_out", vp),
+        ("num_peers", i32),
+        ("reserved", i32),
     ]
 
 
@@ -74,6 +77,9 @@ SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
     "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
+    "skrp_ipc_get_handle": (i32, [vp, vp, vp]),
+    "skrp_ipc_open_handle": (i32, [vp, i64, vp, vp]),
+    "skrp_ipc_close_handle": (i32, [vp]),
     "skrp_tns_count_lines": (i32, [vp, i64, i64, vp, vp]),
     "skrp_tns_line_starts": (i32, [vp, i64, i64, vp, vp, vp]),
     "skrp_tns_classify": (i32, [vp, i64, vp, i64, i64, vp, vp, vp]),

@@ -46,7 +46,7 @@ int skrp_last_error(char *buf, size_t len)
     return skrp::g_err_code;
 }
 
-int skrp_abi_version(void) { return 3; }
+int skrp_abi_version(void) { return 4; }
 
 int skrp_device_sm_count(int *out)
 {
@@ -54,6 +54,53 @@ int skrp_device_sm_count(int *out)
     int dev = 0;
     SKRP_CUDA(cudaGetDevice(&dev));
     SKRP_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev));
+    return SKRP_OK;
+}
+
+// ------------------------------------------------------------- CUDA IPC
+// Peer output buffers for the fused all-gather push: a torch allocation is a
+// slice of a larger cudaMalloc segment, so the handle is taken on the
+// segment base (cuMemGetAddressRange through the runtime's driver entry
+// point -- no -lcuda) and the slice offset travels with it.
+typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
+
+int skrp_ipc_get_handle(const void *dev_ptr, uint8_t *handle64, int64_t *offset)
+{
+    SKRP_REQUIRE(dev_ptr && handle64 && offset, "skrp_ipc_get_handle: null pointer");
+    static MemGetAddressRangeFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        SKRP_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+        SKRP_REQUIRE(f && q == cudaDriverEntryPointSuccess, "cuMemGetAddressRange unavailable");
+        fn = (MemGetAddressRangeFn)f;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    SKRP_REQUIRE(fn(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) == 0, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    SKRP_CUDA(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    return SKRP_OK;
+}
+
+int skrp_ipc_open_handle(const uint8_t *handle64, int64_t offset, void **dev_ptr, void **base_out)
+{
+    SKRP_REQUIRE(handle64 && dev_ptr && base_out && offset >= 0, "skrp_ipc_open_handle: bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    void *base = nullptr;
+    SKRP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *base_out = base;
+    *dev_ptr = (void *)((uintptr_t)base + (uintptr_t)offset);
+    return SKRP_OK;
+}
+
+int skrp_ipc_close_handle(void *base)
+{
+    SKRP_REQUIRE(base != nullptr, "skrp_ipc_close_handle: null pointer");
+    SKRP_CUDA(cudaIpcCloseMemHandle(base));
     return SKRP_OK;
 }
 

@@ -470,7 +470,8 @@ struct PanelVariant {
 template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0>
 static PanelVariant mkp()
 {
-    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF>, NW, 8 * LPN, panel_stage_bytes<8 * LPN, NW>()};
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF>, NW, 8 * LPN,
+                        panel_stage_bytes<8 * LPN, NW, ALG>()};
 }
 
 static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
@@ -485,6 +486,7 @@ static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
     if (nmodes == 3 && rank == 32 && variant == 5) return mkp<3, 4, 2, 16, 0, 1>();
     if (nmodes == 3 && rank == 32 && variant == 6) return mkp<3, 4, 8, 16, 0, 1>();
     if (nmodes == 3 && rank == 32 && variant == 7) return mkp<3, 4, 4, 16, 0, 0, 1>();  // L2 prefetch
+    if (nmodes == 3 && rank == 32 && variant == 8) return mkp<3, 4, 4, 16, 0, 2>();  // one-step staging
     if (nmodes == 3) {
         switch (rank) {
         case 8: return mkp<3, 1, 1, 16>();
@@ -600,6 +602,8 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
     SKRP_REQUIRE(a.factor_ld == 0 || (a.factor_ld >= a.rank && a.factor_ld % 8 == 0), "bad factor_ld %d", a.factor_ld);
     SKRP_REQUIRE(a.out_ld == 0 || (a.out_ld >= a.rank && a.out_ld % 4 == 0), "bad out_ld %d", a.out_ld);
     SKRP_REQUIRE(p.item_rows && p.item_offsets && a.out && a.values && a.work_counter, "null pointer");
+    SKRP_REQUIRE(p.num_peers >= 0 && p.num_peers <= 64 && (p.num_peers == 0 || p.peer_out),
+                 "bad peer output table (%d peers)", p.num_peers);
     for (int w = 0; w < a.nmodes; ++w) {
         SKRP_REQUIRE(a.coords[w] && (w == a.mode || a.factors[w]), "null coordinate/factor pointer (mode %d)", w);
         SKRP_REQUIRE(w == a.mode || aligned(a.factors[w], 32), "factor %d must be 32-byte aligned", w);

@@ -63,9 +63,13 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int slab_rows = pa.slab_rows;
+    // ALG 2 stages only one step of S nonzeros (the S slots) for class-2
+    // batches, so the staging area shrinks 3.7x and the SM keeps its L1 for
+    // the gathers in flight
+    constexpr int SROWS = ALG == 2 ? S : 32;
     float *panel = smem_p;                                          // slab_rows x RR
-    float *stage = panel + (size_t)slab_rows * RR + (size_t)wib * (33 * STR);
-    float *carry_row = stage + 32 * STR;
+    float *stage = panel + (size_t)slab_rows * RR + (size_t)wib * ((SROWS + 1) * STR);
+    float *carry_row = stage + SROWS * STR;
     __shared__ PanelSmem ctl;
     const int slot = lane / LPN, sl = lane % LPN;
     const int col = sl * VEC;
@@ -347,12 +351,25 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                         if (slot == 0) store_vec<VEC>(carry_row + col, acc);
                     }
                 }
+                // ALG 2 class-2 state: the open row and its column-layout run
+                float c2run[CPL];
+                uint32_t c2row = cur;
+                if constexpr (ALG == 2) {
+                    if (cls == 2) {
+                        __syncwarp();
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) {
+                            const int c = lane + 32 * q;
+                            c2run[q] = (c < RR) ? carry_row[c] : 0.f;
+                        }
+                    }
+                }
                 auto group = [&](int g0) {
                     float gv[U][NIN][VEC];
                     float vv[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int e = g0 + slot * U + u;
+                        const int e = g0 + (ALG == 2 ? u * S + slot : slot * U + u);
                         vv[u] = __shfl_sync(kFull, v_l, e);
 #pragma unroll
                         for (int j = 0; j < NIN; ++j) {
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                     } else if (cls == 1) {
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
-                            const bool inA = g0 + slot * U + u < e_b;
+                            const bool inA = g0 + (ALG == 2 ? u * S + slot : slot * U + u) < e_b;
 #pragma unroll
                             for (int i = 0; i < VEC; ++i) {
                                 float p = vv[u];
@@ -383,6 +400,41 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                                 if (inA) acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
                                 else accB[i] = fmaf(p, gv[u][NIN - 1][i], accB[i]);
                             }
+                        }
+                    } else if constexpr (ALG == 2) {
+                        // one step (S consecutive nonzeros) at a time: stage,
+                        // then fold the S rows in order into the open run
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            float p[VEC];
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                p[i] = vv[u];
+#pragma unroll
+                                for (int j = 0; j < NIN; ++j) p[i] *= gv[u][j][i];
+                            }
+                            store_vec<VEC>(stage + slot * STR + col, p);
+                            __syncwarp();
+                            const int e0 = g0 + u * S;
+                            for (int k = 0; k < S && e0 + k < nin; ++k) {
+                                const int e = e0 + k;
+                                if ((cm >> e) & 1u) {
+                                    float *pr = prow(c2row);
+#pragma unroll
+                                    for (int q = 0; q < CPL; ++q) {
+                                        const int c = lane + 32 * q;
+                                        if (c < RR) pr[c] += c2run[q];
+                                        c2run[q] = 0.f;
+                                    }
+                                    c2row = __shfl_sync(kFull, r_l, e);
+                                }
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) {
+                                    const int c = lane + 32 * q;
+                                    if (c < RR) c2run[q] += stage[k * STR + c];
+                                }
+                            }
+                            __syncwarp();
                         }
                     } else {
 #pragma unroll
@@ -408,6 +460,19 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                     cur = __shfl_sync(kFull, r_l, e_b);
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) acc[i] = accB[i];
+                    continue;
+                }
+                if constexpr (ALG == 2) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = lane + 32 * q;
+                        if (c < RR) carry_row[c] = c2run[q];
+                    }
+                    __syncwarp();
+                    cur = c2row;
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
+                    __syncwarp();
                     continue;
                 }
                 // class 2: segmented column sums over the staged rows
@@ -462,8 +527,15 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             const int c4 = (int)(k - r * (RR / 4));
             float4 *src = reinterpret_cast<float4 *>(pbase + r * RR) + c4;
             float *dst = a.out + (size_t)(row_lo + r) * old + 4 * c4;
-            if (additive) red_add_f4(dst, *src);
-            else *reinterpret_cast<float4 *>(dst) = *src;
+            const float4 v = *src;
+            if (additive) red_add_f4(dst, v);
+            else *reinterpret_cast<float4 *>(dst) = v;
+            // fused all-gather: the finished row also goes to every peer's
+            // output buffer (P2P stores over NVLink), so no collective
+            // follows the kernel -- only a completion barrier
+            for (int k = 0; k < pa.num_peers; ++k)
+                *reinterpret_cast<float4 *>(reinterpret_cast<float *>(pa.peer_out[k]) + (size_t)(row_lo + r) * old +
+                                            4 * c4) = v;
             *src = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         if (lockstep) {
@@ -473,8 +545,8 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     }
 }
 
-template <int RR, int NW>
+template <int RR, int NW, int ALG = 0>
 constexpr size_t panel_stage_bytes()
 {
-    return sizeof(float) * NW * (33 * (RR + 4));
+    return sizeof(float) * NW * (((ALG == 2 ? 32 / (RR / 8) : 32) + 1) * (RR + 4));
 }

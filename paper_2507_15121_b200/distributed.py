@@ -127,10 +127,67 @@ class DistributedMttkrp:
         self._rank_r = rank_r
         self.outputs = [torch.empty((p.shape[p.mode], rank_r), dtype=dtype or torch.float32, device=self.device)
                         for p in self.plans]
+        self._close_peers()
+        self._peers = [None] * len(self.plans)
         if self.compute is None:
             for d in range(len(self.plans)):
                 apply_layout(self.plans[d], self.cfg, rank_r, self.mine[d])
                 self._exec(d, rank_r)
+            if self.cfg.fused_allgather and self.world > 1:
+                self._open_peers()
+
+    # ------------------------------------------------- fused all-gather (IPC)
+    def _open_peers(self):
+        """Map every other rank's output buffers (CUDA IPC) for the modes that
+        run the panel kernel: its write-back then stores each finished row to
+        all ranks (NVLink P2P), and the all-gather collective disappears."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        d_ = _dist()
+        self._ipc_bases = []
+        for d, out in enumerate(self.outputs):
+            if self.plans[d].layout != "panel":
+                continue
+            h = (ctypes.c_uint8 * 64)()
+            off = ctypes.c_int64()
+            _lib.call("skrp_ipc_get_handle", out.data_ptr(), h, ctypes.byref(off))
+            allh = [None] * self.world
+            d_.all_gather_object(allh, (bytes(h), int(off.value)), group=self.group)
+            ptrs = []
+            for r, (hb, o) in enumerate(allh):
+                if r == self.rank:
+                    continue
+                ptr, base = ctypes.c_void_p(), ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+                _lib.call("skrp_ipc_open_handle", buf, o, ctypes.byref(ptr), ctypes.byref(base))
+                ptrs.append(ptr.value)
+                self._ipc_bases.append(base.value)
+            table = torch.tensor(np.asarray(ptrs, dtype=np.uint64).view(np.int64), device=self.device)
+            self._peers[d] = (table, len(ptrs))
+
+    def _close_peers(self):
+        from . import _lib
+
+        for b in getattr(self, "_ipc_bases", []):
+            _lib.call("skrp_ipc_close_handle", b)
+        self._ipc_bases = []
+
+    def _peer_sync(self):
+        """All ranks' pushes of this mode are complete before anyone goes on
+        (stream-ordered under NCCL; host barrier under gloo)."""
+        import torch
+
+        d_ = _dist()
+        if d_.get_backend(self.group) == "nccl":
+            t = torch.zeros(1, device=self.device)
+            d_.all_reduce(t, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            d_.barrier(group=self.group)
 
     def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None,
             after_mode=None, outputs=None):
@@ -148,12 +205,19 @@ class DistributedMttkrp:
             out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
                                    out=None if outputs is None else outputs[d])
             if self.world > 1:
-                allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
+                if outputs is None and self._fused(d):
+                    self._peer_sync()  # rows were pushed by every rank's kernel
+                else:
+                    allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
             if after_mode is not None:
                 after_mode(d, out)
             if chained:
                 facs[plan.mode] = out
         return self.outputs
+
+    def _fused(self, d) -> bool:
+        peers = getattr(self, "_peers", None)
+        return bool(peers) and peers[d] is not None
 
     def mode_output(self, d, factors, events=None, out=None):
         """Mode d's MTTKRP on this rank's shards into self.outputs[d] (or
@@ -177,8 +241,12 @@ class DistributedMttkrp:
         else:
             coords, vals = _plan_arrays(plan, self.device)
             stream = torch.cuda.current_stream(self.device)
-            self._exec(d, rank_r).run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg,
-                                      stream.cuda_stream, events=events)
+            ex = self._exec(d, rank_r)
+            if out is self.outputs[d] and self._fused(d):
+                ex.run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg, stream.cuda_stream, events=events,
+                       peers=self._peers[d])
+            else:
+                ex.run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg, stream.cuda_stream, events=events)
         if self.boundary[d]:
             self._reduce_boundary(d, out)
         return out

@@ -73,6 +73,7 @@ class PlatformConfig:
     panel_smem_kb: int = 64     # panel layout: shared memory for the output panel (auto slab size)
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
+    fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -631,7 +632,10 @@ class _PanelExec:
     def launches(self) -> int:
         return 1 if self.num_items else 0
 
-    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None,
+            peers=None):
+        """``peers`` = (device uint64 table of peer output pointers, count):
+        the fused all-gather (every finished row is also stored there)."""
         if self.num_items == 0:
             return
         a = _lib.MttkrpArgs()
@@ -655,6 +659,9 @@ class _PanelExec:
         pa.slab_rows = self.slab_rows
         pa.warps = self.warps
         pa.flags = _lib.PANEL_LOCKSTEP if self.lockstep else 0
+        if peers is not None and peers[1]:
+            pa.peer_out = peers[0].data_ptr()
+            pa.num_peers = peers[1]
         if events is not None:
             events[0].record()
         _lib.check(_lib.lib().skrp_mttkrp_panels(ctypes.byref(a), ctypes.byref(pa), stream), "skrp_mttkrp_panels")

@@ -525,7 +525,7 @@ def test_panel_all_modes_device_invariance(rank):
         facs[d] = results[0][d]
 
 
-@pytest.mark.parametrize("variant", [4, 5])
+@pytest.mark.parametrize("variant", [4, 5, 8])
 def test_panel_slot_variants(variant):
     """Slot-sequential panel ranges (kernel variants 4/5, R=32, N=3): chained
     all-mode parity and bit-identical results for 1 and 3 devices."""

@@ -86,6 +86,23 @@ def _worker(rank, world, port, q):
                     err = np.max(np.abs(outs[d] - expect) / np.maximum(np.abs(expect), 1.0))
                     assert err <= 1e-4, (d, acc, err)
                     facs[d] = outs[d]
+            # fused all-gather: the panel kernel stores every finished row into
+            # the other rank's output buffer (CUDA IPC), no collective follows
+            cfg = sk.PlatformConfig(devices=world, rank=16, layout="panel", fused_allgather=True, panel_l2_mb=0,
+                                    slab_rows=64)
+            lplans = [build_mode_plan_distributed(chunk, d, pcfg) for d in range(len(shape))]
+            runner = DistributedMttkrp(lplans, cfg)
+            outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+            assert all(runner._fused(d) for d in range(len(shape)))
+            facs = [f.data.copy() for f in fs]
+            for d in range(len(shape)):
+                expect = oracle.mttkrp_seq_c(full.indices, full.values, facs, d)
+                err = np.max(np.abs(outs[d] - expect) / np.maximum(np.abs(expect), 1.0))
+                assert err <= 1e-4, (d, "fused", err)
+                facs[d] = outs[d]
+            again = [o.double().cpu().numpy() for o in runner.run(dev_f)]  # buffers reused across steps
+            assert all(np.array_equal(a_, b_) for a_, b_ in zip(outs, again))
+            runner._close_peers()
             # CP-ALS across the two ranks == single process
             als = DistributedCpAls(plans, sk.PlatformConfig(devices=world, rank=16))
             _, lam2, h2 = als.run(dev_f, iterations=2)

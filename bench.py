@@ -658,7 +658,7 @@ def main():
                                                       "memory ('all' or e.g. '0,2'; atomic accumulation)")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
-    ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous"),
+    ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":

@@ -137,7 +137,12 @@ def _prefix(counts, stream):
 
 def build_mode_plan_distributed(chunk, mode: int, cfg: PartitionConfig, scheduling: str = "dynamic",
                                 group=None) -> ModePartitionPlan:
-    """This rank's slice of the mode-`mode` plan from its chunk (see module doc)."""
+    """This rank's slice of the mode-`mode` plan from its chunk (see module doc).
+
+    ``scheduling="split"`` (element-split placement):
+    rank r receives the global sorted positions [r*nnz/m, (r+1)*nnz/m), so a
+    heavy row is cut across ranks exactly like engine.assign_elements cuts a
+    replicated plan -- no rank needs the whole plan."""
     import torch
 
     dist = _dist()
@@ -169,6 +174,10 @@ def build_mode_plan_distributed(chunk, mode: int, cfg: PartitionConfig, scheduli
     bounds_d = torch.from_numpy(bounds).to(dev)
     global_offsets = prefix[bounds_d].cpu().numpy()
     global_sizes = np.diff(global_offsets)
+
+    if scheduling == "split":
+        return _build_split(chunk, mode, cfg, group, coords, vals, counts, prefix, bounds, bounds_d, global_offsets,
+                            global_sizes, t0, stream)
 
     # 3: placement on global sizes (the runner recomputes the same)
     class _Shape:  # minimal plan view for assign_shards
@@ -223,4 +232,91 @@ def build_mode_plan_distributed(chunk, mode: int, cfg: PartitionConfig, scheduli
     plan.global_offsets = global_offsets
     plan.shard_owner = owner
     plan.local_nnz = n_mine
+    return plan
+
+
+def _build_split(chunk, mode, cfg, group, coords, vals, counts, prefix, bounds, bounds_d, global_offsets,
+                 global_sizes, t0, stream):
+    """Split routing: an element of row c with within-row global rank j sits at
+    global sorted position prefix[c] + j; it goes to the rank whose element
+    range holds that position.  Rows inside one range route by their start
+    (skrp_route_by_bounds on the row cuts); only the <= m-1 rows cut by a
+    range edge need j: this rank's rank among the row's elements in its chunk
+    plus the row's counts on lower ranks (an all-gather of m-1 integers)."""
+    import torch
+
+    dist = _dist()
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = vals.device
+    shape = chunk.shape
+    num_indices = shape[mode]
+    n = int(prefix[-1].item())
+    cuts = np.array([r * n // world for r in range(world + 1)], dtype=np.int64)
+    pre_h = prefix.cpu().numpy()
+    # row at global position p: last c with prefix[c] <= p
+    def row_at(p):
+        return int(np.searchsorted(pre_h, p, side="right") - 1)
+
+    inner = [c for c in cuts[1:-1] if 0 < c < n]
+    rcut = [0] + [row_at(c) if 0 < c < n else num_indices for c in cuts[1:-1]] + [num_indices]
+    boundary = sorted({row_at(c) for c in inner if row_at(c - 1) == row_at(c)})
+    # route whole rows by the row cuts (rows [rcut[r], rcut[r+1]) -> r; a cut
+    # row routes to the higher rank here and is fixed up below)
+    n_local = vals.numel()
+    keys = coords[mode]
+    rb = torch.from_numpy(np.asarray(rcut, dtype=np.int64)).to(dev)
+    ident = torch.arange(world, dtype=torch.int32, device=dev)
+    dest = torch.empty(n_local, dtype=torch.int32, device=dev)
+    _lib.call("skrp_route_by_bounds", keys.data_ptr(), n_local, rb.data_ptr(), world, ident.data_ptr(),
+              dest.data_ptr(), stream)
+    if boundary:
+        mine = torch.stack([(keys == b).sum() for b in boundary]).to(torch.int64)
+        allc = [torch.empty_like(mine.cpu()) for _ in range(world)]
+        dist.all_gather(allc, mine.cpu(), group=group)
+        lower = torch.stack(allc[:me]).sum(0) if me else torch.zeros_like(mine.cpu())
+        cuts_d = torch.from_numpy(cuts).to(dev)
+        for bi, b in enumerate(boundary):
+            m = keys == b
+            idx = torch.nonzero(m).squeeze(1)
+            if idx.numel() == 0:
+                continue
+            pos = int(pre_h[b]) + int(lower[bi]) + torch.arange(idx.numel(), device=dev, dtype=torch.int64)
+            dest[idx] = (torch.searchsorted(cuts_d, pos, right=True) - 1).to(torch.int32)
+    send_counts = _histogram(dest, world, stream)
+    _, perm = _stable_sort(dest, max(1, _key_bits(world)), stream)
+    del dest
+    if _backend_is_nccl(group):
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=group)
+    else:
+        gathered = [torch.empty(world, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gathered, send_counts.cpu(), group=group)
+        recv_counts = torch.stack([g[me] for g in gathered]).to(dev)
+    sc = send_counts.cpu().numpy()
+    rcn = recv_counts.cpu().numpy()
+    recv = []
+    for arr in list(coords) + [vals]:
+        moved = _gather(arr, perm, stream)
+        recv.append(_all_to_all(moved, sc, rcn, group))
+        del moved
+    del perm
+    r_coords, r_vals = recv[:-1], recv[-1]
+    bits = _key_bits(num_indices)
+    key_sorted, order = _stable_sort(r_coords[mode], bits, stream)
+    sorted_coords = [key_sorted if w == mode else _gather(r_coords[w], order, stream) for w in range(len(shape))]
+    svals = _gather(r_vals, order, stream)
+    del r_coords, r_vals, order
+    local_counts = _histogram(sorted_coords[mode], num_indices, stream)
+    local_offsets = _prefix(local_counts, stream)[bounds_d].cpu().numpy()
+    torch.cuda.current_stream(dev).synchronize()
+    plan = ModePartitionPlan(mode, shape, cfg.strategy, cfg.isp_capacity, chunk.name, sorted_coords, svals, None,
+                             bounds, local_offsets, build_time=time.perf_counter() - t0)
+    plan.global_shard_nnz = global_sizes
+    plan.global_offsets = global_offsets
+    plan.local_nnz = int(svals.numel())
+    # the element-split placement of the GLOBAL plan (engine.assign_elements)
+    plan.split_info = {"ranges": [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)],
+                       "boundary": boundary, "rcut": rcut}
+    assert plan.local_nnz == int(cuts[me + 1] - cuts[me]), "split routing lost elements"
     return plan

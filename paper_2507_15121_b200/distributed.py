@@ -64,9 +64,15 @@ class DistributedMttkrp:
         self.touch = [None] * len(self.plans)    # rows this rank writes (split)
         if cfg.scheduling == "split":
             for d, p in enumerate(self.plans):
-                ranges, ids, bnd, rcut = assign_elements(p, self.world)
-                self.erange[d] = ranges[self.rank]
-                self.mine[d] = ids[self.rank]
+                info = getattr(p, "split_info", None)
+                if info is not None:  # split-routed distributed plan: local = my element range
+                    bnd, rcut = info["boundary"], info["rcut"]
+                    self.erange[d] = (0, p.nnz)
+                    self.mine[d] = [s_.shard_id for s_ in p.shards if s_.nnz]
+                else:
+                    ranges, ids, bnd, rcut = assign_elements(p, self.world)
+                    self.erange[d] = ranges[self.rank]
+                    self.mine[d] = ids[self.rank]
                 self.boundary[d] = bnd
                 bset = set(bnd)
                 own = []

@@ -135,6 +135,31 @@ def _worker(rank, world, port, q):
             _, lam1, h1 = single.run(dev_f, iterations=2)
             assert np.allclose(h1, h2, atol=1e-4), (h1, h2)
             assert np.allclose(lam1, lam2, rtol=1e-3)
+        # split ROUTING in the distributed build: each rank receives exactly its
+        # element range of the global sorted order (the head row cut across ranks)
+        nnz = full.nnz
+        lo, hi = nnz * rank // world, nnz * (rank + 1) // world
+        fc, fv = full.device_arrays()
+        chunk = sk.SparseTensorCOO.from_device(shape, [c[lo:hi].contiguous() for c in fc], fv[lo:hi].contiguous())
+        pcfg = sk.PartitionConfig(devices=world, strategy="nnz-balanced")
+        ref_plans = sk.build_all_plans(full, pcfg)
+        splans = [build_mode_plan_distributed(chunk, d, pcfg, scheduling="split") for d in range(3)]
+        for d in range(3):
+            e0, e1 = splans[d].split_info["ranges"][rank]
+            assert splans[d].nnz == e1 - e0
+            for w in range(3):  # bit-exact slice of the reference plan order
+                assert torch.equal(splans[d].coords[w], ref_plans[d].coords[w][e0:e1])
+            assert torch.equal(splans[d].vals, ref_plans[d].vals[e0:e1])
+        assert splans[0].split_info["boundary"], "the zipf head row must straddle the split"
+        cfg = sk.PlatformConfig(devices=world, rank=32, accumulation="atomic", scheduling="split", tile_nnz=128)
+        runner = DistributedMttkrp(splans, cfg)
+        outs = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+        facs = [f.data.copy() for f in fs]
+        for d in range(3):
+            expect = oracle.mttkrp_seq_c(full.indices, full.values, facs, d)
+            err = np.max(np.abs(outs[d] - expect) / np.maximum(np.abs(expect), 1.0))
+            assert err <= 1e-4, ("split-routed", d, err)
+            facs[d] = outs[d]
         q.put((rank, "ok"))
     except Exception as exc:  # pragma: no cover
         import traceback

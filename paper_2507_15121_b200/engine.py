@@ -300,6 +300,25 @@ def choose_blocking(plan, rank, shard_ids=None, l2_bytes=96 << 20, max_blocks=64
     return best_sh, best, base
 
 
+def _skewed_rows(plan, shard_ids=None, warps=16) -> bool:
+    """True when one output row holds more than a quarter of a warp's fair
+    share of the nonzeros (#SM x 16 warps): the panel kernel sums a row in one
+    warp, so a Zipf head row would serialise it (cfg4s: 3.2 s per mode); the
+    tile kernel splits such rows across tiles (carries / atomics)."""
+    torch = _torch()
+    ids = range(plan.shard_count) if shard_ids is None else shard_ids
+    nnz = sum(plan.shards[j].nnz for j in ids)
+    if nnz == 0:
+        return False
+    rows = plan.coords[plan.mode]
+    dev = rows.device
+    counts = torch.empty(plan.shape[plan.mode], dtype=torch.int64, device=dev)
+    _lib.call("skrp_histogram", rows.data_ptr(), rows.numel(), counts.numel(), counts.data_ptr(),
+              torch.cuda.current_stream(dev).cuda_stream)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    return int(counts.max().item()) * 4 * sms * warps > nnz
+
+
 def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
@@ -318,7 +337,7 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
                                          max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
     if shifts is not None and (cfg.layout == "blocked" or cost < 0.8 * base):
         if (cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce"
-                and panel_shape(len(plan.shape), rank) is not None):
+                and panel_shape(len(plan.shape), rank) is not None and not _skewed_rows(plan, shard_ids)):
             # deterministic-reduce: the output-stationary panel kernel sums every
             # row in a fixed order with no carry pass, per-group launches or
             # output zeroing -- bit-identical across device counts, 5 % behind

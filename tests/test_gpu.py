@@ -804,3 +804,19 @@ def test_tns_gpu_large_random_file(tmp_path):
     p = sk.build_mode_plan(t_gpu, 0, sk.PartitionConfig())
     q = sk.build_mode_plan(t_cpu, 0, sk.PartitionConfig())
     assert np.array_equal(p.order(), q.order())
+
+
+def test_auto_layout_avoids_panel_on_skewed_rows():
+    """deterministic-reduce + auto layout: the panel kernel sums a row in one
+    warp, so a Zipf head row must route the plan to the tile layout instead;
+    uniform rows take the panel."""
+    from paper_2507_15121_b200.engine import _skewed_rows, apply_layout
+
+    z = sk.synth_tensor_device((2000, 3000, 4000), 2_000_000, distribution="zipf", seed=3)
+    u = sk.synth_tensor_device((200_000, 3000, 4000), 2_000_000, seed=3)
+    pz = sk.build_mode_plan(z, 0, sk.PartitionConfig(strategy="nnz-balanced"))
+    pu = sk.build_mode_plan(u, 0, sk.PartitionConfig())
+    assert _skewed_rows(pz) and not _skewed_rows(pu)
+    cfg = sk.PlatformConfig(rank=32, accumulation="deterministic-reduce", layout="auto", l2_budget_mb=0)
+    apply_layout(pz, cfg, 32)
+    assert pz.layout != "panel"

@@ -333,11 +333,16 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
         if cfg.layout == "blocked":
             raise ValueError("blocked layout needs R in {8,16,32,64,128} and N <= 5")
         return plan
+    if cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce" and _skewed_rows(plan, shard_ids):
+        # skewed rows under deterministic-reduce: plan order + carry tree runs at
+        # the atomic speed (cfg4s 28.4 vs 29.2 ms/step, cfg5s 56.6 vs 56.7),
+        # the blocked carry path pays per-group launches (123 / 191 ms)
+        return plan
     shifts, cost, base = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20,
                                          max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
     if shifts is not None and (cfg.layout == "blocked" or cost < 0.8 * base):
         if (cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce"
-                and panel_shape(len(plan.shape), rank) is not None and not _skewed_rows(plan, shard_ids)):
+                and panel_shape(len(plan.shape), rank) is not None):
             # deterministic-reduce: the output-stationary panel kernel sums every
             # row in a fixed order with no carry pass, per-group launches or
             # output zeroing -- bit-identical across device counts, 5 % behind

@@ -293,7 +293,7 @@ def run_ours(args, cfg):
 
     shape, nnz, R = cfg["shape"], cfg["nnz"], cfg["rank"]
     modes = list(range(len(shape))) if cfg["modes"] is None else cfg["modes"]
-    pcfg = sk.PartitionConfig(devices=world, strategy=cfg["strategy"])
+    pcfg = sk.PartitionConfig(devices=max(world, args.emulate_world), strategy=cfg["strategy"])
     pl = sk.PlatformConfig(devices=world, rank=R, accumulation=args.accumulation, tile_nnz=args.tile,
                            scheduling=args.scheduling,
                            kernel_variant=args.variant,
@@ -336,6 +336,8 @@ def run_ours(args, cfg):
         for i in streamed:
             plans[i].to_host()
         torch.cuda.empty_cache()
+    if args.emulate_world > 1:
+        return emulate_world(args, cfg, plans, pl, dev_f, dev, build_s)
     runner = DistributedMttkrp(plans, pl, rank=rank, world=world, device=dev)
     runner.prepare(R)
     setup_s = time.perf_counter() - t_setup
@@ -480,6 +482,54 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return 0
+
+
+def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
+    """Projected N-GPU step on ONE GPU (no multi-GPU box here): the plans are
+    built for N devices; every rank's share (its shards, placement as the real
+    N-rank run) is timed alone on this GPU, compute only; the per-mode
+    all-gather is modelled as (N-1)/N of the output bytes entering each GPU at
+    `link_gbs` (775 GB/s: measured kernel P2P rate on NVLink5 in
+    B300_MICROARCH.md).  Prints one JSON line, kind "emulated"."""
+    import torch
+
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    n = args.emulate_world
+    shape, R = cfg["shape"], cfg["rank"]
+    modes = list(range(len(shape))) if cfg["modes"] is None else cfg["modes"]
+    import dataclasses
+
+    plcfg = dataclasses.replace(pl, devices=n)
+    per_rank = []
+    for r in range(n):
+        runner = DistributedMttkrp(plans, plcfg, rank=r, world=n, device=dev)
+        runner.prepare(R)
+        for _ in range(args.warmup):
+            runner.run(dev_f, exchange=False)
+        kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in modes]
+               for _ in range(args.steps)]
+        for k in range(args.steps):
+            runner.run(dev_f, kernel_events=kev[k], exchange=False)
+        torch.cuda.synchronize()
+        per_mode = [sum(kev[k][i][0].elapsed_time(kev[k][i][1]) for k in range(args.steps)) / args.steps
+                    for i in range(len(modes))]
+        per_rank.append(per_mode)
+        del runner
+    gather_ms = [(n - 1) / n * shape[d] * R * 4 / (link_gbs * 1e9) * 1e3 for d in modes]
+    step_ms = sum(max(pr[i] for pr in per_rank) + gather_ms[i] for i in range(len(modes)))
+    line = {"kind": "emulated", "metric": METRIC, "n_gpus_emulated": n, "unit": "nnz/s",
+            "value_projected": len(modes) * cfg["nnz"] / (step_ms / 1e3), "ms_per_step_projected": step_ms,
+            "per_rank_kernel_ms_per_mode": per_rank, "allgather_ms_per_mode_modelled": gather_ms,
+            "link_gbs_assumed": link_gbs,
+            "config": {"workload": cfg["desc"], "partition": f"{cfg['strategy']}, devices={n}, oversub 4",
+                       "scheduling": args.scheduling, "accumulation": args.accumulation,
+                       "layout": [p.layout for p in plans]},
+            "method": "each rank's shards timed alone on one B200 (compute only, CUDA events), max over ranks "
+                      "per mode + modelled all-gather; not a multi-GPU measurement",
+            "plan_build_seconds": build_s}
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -656,6 +706,8 @@ def main():
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
     ap.add_argument("--stream-modes", default="", help="out-of-core: stream these modes' plans from pinned host "
                                                       "memory ('all' or e.g. '0,2'; atomic accumulation)")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),

@@ -196,11 +196,13 @@ class DistributedMttkrp:
             d_.barrier(group=self.group)
 
     def run(self, factors, chained=True, kernel_events=None, ledger: TransferLedger | None = None,
-            after_mode=None, outputs=None):
+            after_mode=None, outputs=None, exchange=True):
         """All modes; `factors` are this rank's full fp32 factor replicas.
         Returns the list of gathered outputs (device tensors, reused).
         ``after_mode(i, out)`` is called once mode i's output is gathered
-        (stream-ordered), e.g. to start its device-to-host copy."""
+        (stream-ordered), e.g. to start its device-to-host copy.
+        ``exchange=False`` skips the all-gather (one rank's compute alone:
+        bench.py --emulate-world runs every rank's share on one GPU)."""
         import torch
 
         rank_r = factors[0].shape[1]
@@ -210,7 +212,7 @@ class DistributedMttkrp:
         for d, plan in enumerate(self.plans):
             out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
                                    out=None if outputs is None else outputs[d])
-            if self.world > 1:
+            if self.world > 1 and exchange:
                 if outputs is None and self._fused(d):
                     self._peer_sync()  # rows were pushed by every rank's kernel
                 else:

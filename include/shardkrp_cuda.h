@@ -203,6 +203,23 @@ int skrp_tns_parse(const uint8_t *text, int64_t n, const int64_t *starts, int64_
  * grammar (the caller parses it). */
 int skrp_tns_parse_token_host(const char *tok, int64_t len, int32_t as_int, int64_t *ival, double *dval);
 
+/* ------------------------------------ GPU-direct plan cache (§8(f) row 4)
+ * The reference's v1 plan file (partition.py:265-379) moves between disk and
+ * HBM without host array work.  CRC32 (zlib): raw_crcs[i] = CRC register
+ * after sub-chunk i of `data` starting from 0 (no inversions), on the GPU;
+ * fold_host combines them in order into zlib.crc32(data, crc_in).  Indices:
+ * u64 AoS (nrec x nmodes) <-> one u32 array per mode (*bad_count += values
+ * >= 2^32).  Values: f64 -> f32 for the device copy. */
+int skrp_crc32_chunks(const uint8_t *data, int64_t n, int64_t sub_len, uint32_t *raw_crcs, skrp_stream_t stream);
+int skrp_crc32_fold_host(const uint32_t *raw_crcs, int64_t count, int64_t sub_len, int64_t total_len,
+                         uint32_t crc_in, uint32_t *crc_out);
+int skrp_crc32_raw_host(const uint8_t *data, int64_t n, uint32_t *out);
+int skrp_plan_unpack_indices(const uint64_t *aos, int64_t nrec, int32_t nmodes, uint32_t *const *coords,
+                             unsigned long long *bad_count, skrp_stream_t stream);
+int skrp_plan_pack_indices(const uint32_t *const *coords, int64_t nrec, int32_t nmodes, uint64_t *aos,
+                           skrp_stream_t stream);
+int skrp_f64_to_f32(const double *in, int64_t n, float *out, skrp_stream_t stream);
+
 /* Column planes for column-pass execution (B200 addition, no reference
  * counterpart): dst (parts x rows x rank/parts, fp32) plane p = columns
  * [p*rank/parts, (p+1)*rank/parts) of src (rows x rank, row-major).  A pass

@@ -77,6 +77,12 @@ SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
     "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
+    "skrp_crc32_chunks": (i32, [vp, i64, i64, vp, vp]),
+    "skrp_crc32_fold_host": (i32, [vp, i64, i64, i64, ctypes.c_uint32, vp]),
+    "skrp_crc32_raw_host": (i32, [vp, i64, vp]),
+    "skrp_plan_unpack_indices": (i32, [vp, i64, i32, vp, vp, vp]),
+    "skrp_plan_pack_indices": (i32, [vp, i64, i32, vp, vp]),
+    "skrp_f64_to_f32": (i32, [vp, i64, vp, vp]),
     "skrp_ipc_get_handle": (i32, [vp, vp, vp]),
     "skrp_ipc_open_handle": (i32, [vp, i64, vp, vp]),
     "skrp_ipc_close_handle": (i32, [vp]),

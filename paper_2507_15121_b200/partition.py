@@ -171,6 +171,8 @@ class ModePartitionPlan:
 
     @property
     def value_dtype(self):
+        if getattr(self, "_file_src", None) is not None:
+            return self._file_src["dtype"]
         if self._source is not None and self._source._values is not None:
             return self._source._values.dtype
         return np.dtype(np.float32)
@@ -190,8 +192,19 @@ class ModePartitionPlan:
             raise ValueError("plan was built with keep_permutation=False")
         return self.perm.cpu().numpy().astype(np.int64)
 
+    def _file_view(self, what):
+        """Host views of a plan loaded from a cache file: memory-mapped from
+        the file itself (exact stored values, no HBM round trip)."""
+        f = self._file_src
+        if what == "idx":
+            return np.memmap(f["path"], dtype=INDEX_DTYPE, mode="r", offset=f["idx_off"],
+                             shape=(f["nnz"], f["nmodes"]))
+        return np.memmap(f["path"], dtype=f["dtype"], mode="r", offset=f["val_off"], shape=(f["nnz"],))
+
     @property
     def _indices(self) -> np.ndarray:
+        if self._host_idx is None and getattr(self, "_file_src", None) is not None and self.layout == "flycoo":
+            self._host_idx = np.asarray(self._file_view("idx"))
         if self._host_idx is None:
             src = self._source
             if src is not None and src._indices is not None and self.perm is not None:
@@ -205,6 +218,8 @@ class ModePartitionPlan:
 
     @property
     def _values(self) -> np.ndarray:
+        if self._host_vals is None and getattr(self, "_file_src", None) is not None and self.layout == "flycoo":
+            self._host_vals = np.asarray(self._file_view("val"))
         if self._host_vals is None:
             src = self._source
             if src is not None and src._values is not None and self.perm is not None:
@@ -621,9 +636,12 @@ _VALUE_TAG = {np.dtype(np.float64): 8, np.dtype(np.float32): 4}
 _TAG_VALUE = {v: k for k, v in _VALUE_TAG.items()}
 
 
-def save_plan(plan: ModePartitionPlan, path):
+_CRC_SUB = 1 << 12        # CRC sub-chunk (bytes) computed per GPU thread
+_IO_RECORDS = 1 << 22     # index records / values per streamed chunk
+
+
+def _header(plan) -> bytes:
     import struct
-    import zlib
 
     body = bytearray()
     body += struct.pack("<I", PLAN_VERSION)
@@ -636,30 +654,125 @@ def save_plan(plan: ModePartitionPlan, path):
     body += struct.pack("<I", plan.shard_count)
     name = plan.name.encode("utf-8")
     body += struct.pack("<I", len(name)) + name
-    for s in plan.shards:
-        body += struct.pack("<QQQ", s.index_range[0], s.index_range[1], s.nnz)
+    for sh in plan.shards:
+        body += struct.pack("<QQQ", sh.index_range[0], sh.index_range[1], sh.nnz)
+    return bytes(body)
+
+
+def _crc_device(buf, n, crc, stream):
+    """zlib.crc32 continued over the first n bytes of device buffer `buf`:
+    per-thread raw CRCs of 4-KB sub-chunks on the GPU, folded on the host."""
+    import ctypes
+
+    import torch
+
+    if n == 0:
+        return crc
+    cnt = -(-n // _CRC_SUB)
+    raws = torch.empty(cnt, dtype=torch.int32, device=buf.device)
+    _lib.call("skrp_crc32_chunks", buf.data_ptr(), n, _CRC_SUB, raws.data_ptr(), stream)
+    h = raws.cpu().numpy()
+    out = ctypes.c_uint32()
+    _lib.call("skrp_crc32_fold_host", h.ctypes.data, cnt, _CRC_SUB, n, crc & 0xFFFFFFFF, ctypes.byref(out))
+    return out.value
+
+
+def save_plan(plan: ModePartitionPlan, path):
+    """Write the reference's v1 plan file (partition.py:270-292), byte-for-byte
+    the same layout.  GPU-direct: the u64 AoS index section is packed from the
+    device coordinates and checksummed on the GPU, then streamed to disk;
+    values come from their exact source (host f64 or the device f32 copy)."""
+    import struct
+    import zlib
+
+    import torch
+
+    if plan.layout != "flycoo" or plan.coords is None:
+        return _save_plan_host(plan, path)
+    dev = plan.vals.device
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    nm, nnz = len(plan.shape), plan.nnz
+    head = _header(plan)
+    crc = zlib.crc32(head)
+    dtype = np.dtype(plan.value_dtype)
+    with open(path, "wb") as fh:
+        fh.write(PLAN_MAGIC)
+        fh.write(head)
+        aos = torch.empty(min(nnz, _IO_RECORDS) * nm, dtype=torch.int64, device=dev)
+        host = torch.empty(aos.numel(), dtype=torch.int64, pin_memory=True)
+        for r0 in range(0, nnz, _IO_RECORDS):
+            k = min(_IO_RECORDS, nnz - r0)
+            cptr = (_lib.vp * nm)(*[c.data_ptr() + 4 * r0 for c in plan.coords])
+            _lib.call("skrp_plan_pack_indices", cptr, k, nm, aos.data_ptr(), stream)
+            crc = _crc_device(aos, k * nm * 8, crc, stream)
+            host[:k * nm].copy_(aos[:k * nm])
+            fh.write(host[:k * nm].numpy().tobytes())
+        if dtype == np.float32 and getattr(plan, "_file_src", None) is None and (
+                plan._source is None or plan._source._values is None):
+            for r0 in range(0, nnz, _IO_RECORDS):
+                k = min(_IO_RECORDS, nnz - r0)
+                chunk = plan.vals[r0:r0 + k]
+                crc = _crc_device(chunk, k * 4, crc, stream)
+                fh.write(chunk.cpu().numpy().tobytes())
+        else:  # exact stored dtype from the host source (f64 values never round-trip through fp32)
+            vals = np.ascontiguousarray(plan._values, dtype=dtype)
+            for r0 in range(0, nnz, _IO_RECORDS):
+                b = vals[r0:r0 + _IO_RECORDS].tobytes()
+                crc = zlib.crc32(b, crc)
+                fh.write(b)
+        fh.write(struct.pack("<I", crc & 0xFFFFFFFF))
+
+
+def _save_plan_host(plan, path):
+    import struct
+    import zlib
+
+    body = bytearray(_header(plan))
     body += np.ascontiguousarray(plan._indices, dtype=INDEX_DTYPE).tobytes()
-    body += np.ascontiguousarray(plan._values).tobytes()
+    body += np.ascontiguousarray(plan._values, dtype=plan.value_dtype).tobytes()
     with open(path, "wb") as fh:
         fh.write(PLAN_MAGIC)
         fh.write(body)
         fh.write(struct.pack("<I", zlib.crc32(bytes(body))))
 
 
-def load_plan(path, value_dtype=None, *, device=None) -> ModePartitionPlan:
-    """Read a v1 plan file (checksum + version validated) and upload it."""
-    import struct
+def _file_crc_host(path, size):
     import zlib
+
+    crc = 0
+    with open(path, "rb") as fh:
+        fh.seek(len(PLAN_MAGIC))
+        left = size - len(PLAN_MAGIC) - 4
+        while left > 0:
+            b = fh.read(min(left, 1 << 26))
+            if not b:
+                break
+            crc = zlib.crc32(b, crc)
+            left -= len(b)
+    return crc & 0xFFFFFFFF
+
+
+def load_plan(path, value_dtype=None, *, device=None) -> ModePartitionPlan:
+    """Read a v1 plan file (partition.py:295-379: checksum, then version and
+    value-type checks, same exceptions) straight into HBM.  GPU-direct: the
+    index and value sections stream through a pinned buffer into device
+    staging buffers where the GPU checksums them (4-KB sub-chunk CRCs folded
+    on the host) and splits the u64 AoS records into per-mode u32 arrays;
+    host views (_indices / _values) are memory-mapped from the file."""
+    import os
+    import struct
 
     import torch
 
+    size = os.path.getsize(path)
     with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < len(PLAN_MAGIC) + 4 or blob[: len(PLAN_MAGIC)] != PLAN_MAGIC:
+        head = fh.read(min(size, 1 << 22))
+    if size < len(PLAN_MAGIC) + 4 or head[:len(PLAN_MAGIC)] != PLAN_MAGIC:
         raise PlanVersionError(f"{path}: not a plan cache file")
-    body = blob[len(PLAN_MAGIC):-4]
-    if zlib.crc32(body) != struct.unpack("<I", blob[-4:])[0]:
-        raise PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)")
+    with open(path, "rb") as fh:
+        fh.seek(size - 4)
+        (crc_stored,) = struct.unpack("<I", fh.read(4))
+    body = head[len(PLAN_MAGIC):]
     pos = 0
 
     def take(fmt):
@@ -668,35 +781,78 @@ def load_plan(path, value_dtype=None, *, device=None) -> ModePartitionPlan:
         pos += struct.calcsize(fmt)
         return out
 
-    (version,) = take("<I")
+    def integrity_then(exc):
+        # the reference checks the CRC before anything else
+        if _file_crc_host(path, size) != crc_stored:
+            raise PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)")
+        raise exc
+
+    try:
+        (version,) = take("<I")
+        (vtag,) = take("<B")
+        (stag,) = take("<B")
+        (mode,) = take("<I")
+        (nmodes,) = take("<I")
+        shape = take(f"<{nmodes}Q")
+        nnz, capacity, build_time = take("<QQd")
+        (shards,) = take("<I")
+        (nlen,) = take("<I")
+        name = body[pos:pos + nlen].decode("utf-8")
+        pos += nlen
+        table = np.array([take("<QQQ") for _ in range(shards)], dtype=np.int64).reshape(-1, 3)
+    except (struct.error, UnicodeDecodeError, ValueError, MemoryError):
+        integrity_then(PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)"))
     if version != PLAN_VERSION:
-        raise PlanVersionError(f"{path}: plan version {version}, expected {PLAN_VERSION}")
-    (vtag,) = take("<B")
+        integrity_then(PlanVersionError(f"{path}: plan version {version}, expected {PLAN_VERSION}"))
     if vtag not in _TAG_VALUE:
-        raise PlanVersionError(f"{path}: unknown value-type tag {vtag}")
+        integrity_then(PlanVersionError(f"{path}: unknown value-type tag {vtag}"))
     dtype = _TAG_VALUE[vtag]
     if value_dtype is not None and np.dtype(value_dtype) != dtype:
-        raise PlanVersionError(f"{path}: plan stores {dtype} values, expected {np.dtype(value_dtype)}")
-    (stag,) = take("<B")
-    (mode,) = take("<I")
-    (nmodes,) = take("<I")
-    shape = take(f"<{nmodes}Q")
-    nnz, capacity, build_time = take("<QQd")
-    (shards,) = take("<I")
-    (nlen,) = take("<I")
-    name = body[pos:pos + nlen].decode("utf-8")
-    pos += nlen
-    table = np.array([take("<QQQ") for _ in range(shards)], dtype=np.int64).reshape(-1, 3)
-    idx = np.frombuffer(body, dtype=INDEX_DTYPE, count=nnz * nmodes, offset=pos).reshape(nnz, nmodes)
-    pos += nnz * nmodes * 8
-    vals = np.frombuffer(body, dtype=dtype, count=nnz, offset=pos)
+        integrity_then(PlanVersionError(f"{path}: plan stores {dtype} values, expected {np.dtype(value_dtype)}"))
+    hdr_len = pos
+    idx_off = len(PLAN_MAGIC) + hdr_len
+    val_off = idx_off + nnz * nmodes * 8
+    if val_off + nnz * dtype.itemsize + 4 != size or any(x >= 2 ** 32 for x in shape):
+        integrity_then(PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)"))
+
+    gpu = device or torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(gpu).cuda_stream
+    import zlib
+
+    crc = zlib.crc32(body[:hdr_len])
+    coords = [torch.empty(nnz, dtype=torch.int32, device=gpu) for _ in range(nmodes)]
+    dvals = torch.empty(nnz, dtype=torch.float32, device=gpu)
+    rec = nmodes * 8
+    k_max = max(1, min(nnz, _IO_RECORDS))
+    pinned = torch.empty(k_max * max(rec, 8), dtype=torch.uint8, pin_memory=True)
+    stage = torch.empty(k_max * max(rec, 8), dtype=torch.uint8, device=gpu)
+    bad = torch.zeros(1, dtype=torch.int64, device=gpu)
+    with open(path, "rb") as fh:
+        fh.seek(idx_off)
+        for r0 in range(0, nnz, _IO_RECORDS):
+            k = min(_IO_RECORDS, nnz - r0)
+            n = fh.readinto(pinned[:k * rec].numpy())
+            stage[:n].copy_(pinned[:n], non_blocking=True)
+            crc = _crc_device(stage, k * rec, crc, stream)
+            cptr = (_lib.vp * nmodes)(*[c.data_ptr() + 4 * r0 for c in coords])
+            _lib.call("skrp_plan_unpack_indices", stage.data_ptr(), k, nmodes, cptr, bad.data_ptr(), stream)
+        for r0 in range(0, nnz, _IO_RECORDS):
+            k = min(_IO_RECORDS, nnz - r0)
+            n = fh.readinto(pinned[:k * dtype.itemsize].numpy())
+            stage[:n].copy_(pinned[:n], non_blocking=True)
+            crc = _crc_device(stage, k * dtype.itemsize, crc, stream)
+            if dtype == np.float64:
+                _lib.call("skrp_f64_to_f32", stage.data_ptr(), k, dvals.data_ptr() + 4 * r0, stream)
+            else:
+                dvals[r0:r0 + k].copy_(stage[:k * 4].view(torch.float32))
+    if (crc & 0xFFFFFFFF) != crc_stored:
+        raise PlanIntegrityError(f"{path}: checksum mismatch (truncated or corrupted)")
+    if int(bad.item()):
+        raise ValueError(f"{path}: indices >= 2^32 cannot live on the device")
     bounds = np.concatenate([table[:, 0], table[-1:, 1]]) if shards else np.zeros(1, dtype=np.int64)
     offsets = np.concatenate([[0], np.cumsum(table[:, 2])]).astype(np.int64)
-    gpu = device or torch.device("cuda", torch.cuda.current_device())
-    coords = [torch.from_numpy(idx[:, w].astype(np.int32)).to(gpu) for w in range(nmodes)]
-    dvals = torch.from_numpy(vals.astype(np.float32)).to(gpu)
-    plan = ModePartitionPlan(int(mode), tuple(int(s) for s in shape), STRATEGIES[stag], int(capacity), name,
+    plan = ModePartitionPlan(int(mode), tuple(int(x) for x in shape), STRATEGIES[stag], int(capacity), name,
                              coords, dvals, None, bounds, offsets, build_time=float(build_time))
-    plan._host_idx = idx
-    plan._host_vals = vals
+    plan._file_src = {"path": os.fspath(path), "idx_off": idx_off, "val_off": val_off, "nnz": int(nnz),
+                      "nmodes": int(nmodes), "dtype": dtype}
     return plan

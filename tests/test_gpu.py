@@ -820,3 +820,77 @@ def test_auto_layout_avoids_panel_on_skewed_rows():
     cfg = sk.PlatformConfig(rank=32, accumulation="deterministic-reduce", layout="auto", l2_budget_mb=0)
     apply_layout(pz, cfg, 32)
     assert pz.layout == "flycoo"  # plan order + carry tree: the fast deterministic path on skewed rows
+
+
+# ------------------------------------------------------------- plan cache v1
+
+
+def test_plan_cache_reference_files(golden, tmp_path):
+    """GPU-direct load_plan of files written by the REFERENCE's save_plan
+    (tests/golden/make_plan_golden.py): same shards, ISPs, host views
+    (bit-exact, stored dtype) and device arrays as our own build; our
+    save_plan reproduces the reference file byte-for-byte (from a fresh
+    build and from the loaded plan); corruption / truncation / version /
+    dtype errors are the reference's."""
+    import json
+    import os
+
+    gdir = os.path.join(os.path.dirname(__file__), "golden", "plans")
+    with open(os.path.join(gdir, "index.json")) as fh:
+        index = json.load(fh)
+    s = golden("synth.npz")
+    for e in index:
+        path = os.path.join(gdir, e["file"])
+        raw = open(path, "rb").read()
+        p = sk.load_plan(path)
+        name = e["tensor"]
+        t = sk.SparseTensorCOO(tuple(int(x) for x in s[f"{name}_shape"]), s[f"{name}_indices"],
+                               s[f"{name}_values"].astype(e["dtype"]), name=name)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            ref = sk.build_mode_plan(t, e["mode"], sk.PartitionConfig(devices=e["devices"], strategy=e["strategy"],
+                                                                       isp_capacity=e["isp_capacity"]))
+        assert [(x.index_range, x.nnz) for x in p.shards] == [(x.index_range, x.nnz) for x in ref.shards]
+        assert all(np.array_equal(a.isp_boundaries, b.isp_boundaries) for a, b in zip(p.shards, ref.shards))
+        assert np.array_equal(p._indices, ref._indices)
+        assert p._values.dtype == np.dtype(e["dtype"]) and p._values.tobytes() == ref._values.tobytes()
+        for w in range(len(t.shape)):
+            assert torch.equal(p.coords[w], ref.coords[w])
+        assert torch.equal(p.vals, ref.vals)
+        ref.build_time = e["build_time"]
+        sk.save_plan(ref, tmp_path / "a.plan")
+        assert (tmp_path / "a.plan").read_bytes() == raw, e["file"]
+        sk.save_plan(p, tmp_path / "b.plan")
+        assert (tmp_path / "b.plan").read_bytes() == raw, e["file"]
+        # loaded plans run the kernel
+        fs = sk.random_factors(t.shape, 8, seed=1)
+        cfg = sk.PlatformConfig(devices=2, rank=8)
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+        expect = oracle.mttkrp_seq(t.indices, t.values, [f.data for f in fs], e["mode"])
+        assert rel_err(out, expect) <= TOL
+    # errors, in the reference's order (checksum first)
+    path = os.path.join(gdir, index[0]["file"])
+    raw = bytearray(open(path, "rb").read())
+    bad = tmp_path / "bad.plan"
+    flipped = bytearray(raw)
+    flipped[len(raw) // 2] ^= 0xFF
+    bad.write_bytes(bytes(flipped))
+    with pytest.raises(sk.PlanIntegrityError):
+        sk.load_plan(bad)
+    bad.write_bytes(bytes(raw[:-100]))
+    with pytest.raises(sk.PlanIntegrityError):
+        sk.load_plan(bad)
+    bad.write_bytes(b"not a plan at all")
+    with pytest.raises(sk.PlanVersionError):
+        sk.load_plan(bad)
+    with pytest.raises(sk.PlanVersionError, match="expected float32"):
+        sk.load_plan(path, value_dtype=np.float32)
+    import struct
+    import zlib
+
+    v2 = bytearray(raw)
+    v2[8:12] = struct.pack("<I", 2)
+    v2[-4:] = struct.pack("<I", zlib.crc32(bytes(v2[8:-4])))
+    bad.write_bytes(bytes(v2))
+    with pytest.raises(sk.PlanVersionError, match="plan version 2"):
+        sk.load_plan(bad)

@@ -349,3 +349,30 @@ def test_gpu_float_parser_matches_python_float():
         assert L.skrp_tns_parse_token_host(b, len(b), 1, ctypes.byref(iv), ctypes.byref(dv)) == ok
         if not ok:
             assert iv.value == int(tok)
+
+
+def test_crc32_fold_matches_zlib():
+    """The plan-cache checksum path: raw sub-chunk CRCs (computed on the GPU
+    in production; host twin here) folded with the GF(2) shift operator ==
+    zlib.crc32, for any length, sub-chunk size and starting crc."""
+    import zlib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(0)
+    out = ctypes.c_uint32()
+    for n, sub in [(0, 16), (1, 16), (15, 16), (4097, 16), (100_000, 4096), (1 << 20, 4096), (12345, 48)]:
+        data = rng.integers(0, 256, n, dtype=np.uint8)
+        cnt = -(-n // sub)
+        raws = np.zeros(max(cnt, 1), dtype=np.uint32)
+        for i in range(cnt):
+            L.skrp_crc32_raw_host(data[i * sub:].ctypes.data, min(sub, n - i * sub), raws[i:].ctypes.data)
+        for crc_in in (0, 0xDEADBEEF):
+            _lib.call("skrp_crc32_fold_host", raws.ctypes.data, cnt, sub, n, crc_in, ctypes.byref(out))
+            assert out.value == zlib.crc32(data.tobytes(), crc_in)
+
+
+def test_plan_cache_rejects_non_plan_files(tmp_path):
+    p = tmp_path / "x.plan"
+    p.write_bytes(b"definitely not a plan")
+    with pytest.raises(sk.PlanVersionError, match="not a plan cache file"):
+        sk.load_plan(p)

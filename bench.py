@@ -346,6 +346,7 @@ def run_ours(args, cfg):
 
     for _ in range(args.warmup):
         runner.run(dev_f)
+    rebalanced = runner.rebalance(dev_f) if args.rebalance and world > 1 else []
     barrier()
 
     # ---- timed region: K all-mode steps, inputs resident in HBM
@@ -459,6 +460,7 @@ def run_ours(args, cfg):
                        "layout": [p.layout for p in plans],
                        "block_shifts": [p.block_shifts for p in plans],
                        "parallelism": f"output-row shards x{world}", "scheduling": args.scheduling,
+                       "rebalanced_modes": rebalanced,
                        "allgather": ("none (1 GPU)" if world == 1 else
                                      "fused: panel write-back P2P-stores rows into every rank (CUDA IPC)"
                                      if any(runner._fused(i) for i in range(len(modes))) else
@@ -706,6 +708,8 @@ def main():
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
     ap.add_argument("--stream-modes", default="", help="out-of-core: stream these modes' plans from pinned host "
                                                       "memory ('all' or e.g. '0,2'; atomic accumulation)")
+    ap.add_argument("--rebalance", action="store_true",
+                    help="N>1: re-place shards from measured per-GPU kernel times after the warm-up")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",

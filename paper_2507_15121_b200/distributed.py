@@ -95,6 +95,62 @@ class DistributedMttkrp:
         self._execs = {}
         self.outputs = None
 
+    # ----------------------------------------------------------- rebalancing
+    def measure_mode_seconds(self, factors, chained=True):
+        """This rank's kernel seconds per mode (one eager all-mode pass with
+        CUDA events on the launching stream)."""
+        import torch
+
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in self.plans]
+        self.run(factors, chained=chained, kernel_events=ev)
+        torch.cuda.synchronize(self.device)
+        return [a.elapsed_time(b) / 1e3 for a, b in ev]
+
+    def rebalance(self, factors=None, rank_seconds=None):
+        """Host-side rebalancing across the GPUs from MEASURED per-GPU times
+        (SURVEY.md §8(e)): each rank's per-nonzero cost in mode d is its
+        measured kernel time over its nonzeros; a shard is then weighted by
+        nnz x the cost of the GPU that ran it, and the placement (contiguous
+        cut or the dynamic claim replay) is recomputed on those weights -- a
+        GPU that ran slow (heavier rows, worse locality, a slower device)
+        sheds work.  ``rank_seconds[r][d]`` may be given (tests); otherwise
+        every rank measures one pass and the times are all-gathered.  Only
+        replicated plans move (the data of distributed plans stays put);
+        returns the modes whose placement changed."""
+        if rank_seconds is None:
+            mine = self.measure_mode_seconds(factors)
+            if self.world > 1:
+                allt = [None] * self.world
+                _dist().all_gather_object(allt, mine, group=self.group)
+            else:
+                allt = [mine]
+            rank_seconds = allt
+        changed = []
+        for d, p in enumerate(self.plans):
+            if self.cfg.scheduling not in ("contiguous", "dynamic") or getattr(p, "global_shard_nnz", None) is not None:
+                continue
+            owner = np.empty(p.shard_count, dtype=np.int64)
+            for r, ids in enumerate(self.assignment[d]):
+                owner[ids] = r
+            nnz_r = np.array([sum(p.shards[j].nnz for j in ids) for ids in self.assignment[d]], dtype=np.float64)
+            rate = np.array([rank_seconds[r][d] for r in range(self.world)], dtype=np.float64) / np.maximum(nnz_r, 1)
+            if not np.all(rate > 0):
+                continue
+            w = np.array([s_.nnz for s_ in p.shards], dtype=np.float64) * rate[owner]
+            new = assign_shards(p, self.world, self.cfg.scheduling, weights=w)
+            if [list(x) for x in new] != [list(x) for x in self.assignment[d]]:
+                self.assignment[d] = new
+                self.ownership[d] = [_normalize_ranges([p.shards[j].index_range for j in new[r]])
+                                     for r in range(self.world)]
+                self.mine[d] = new[self.rank]
+                for key in [k for k in self._execs if k[0] == d]:
+                    del self._execs[key]
+                changed.append(d)
+        if changed and self.outputs is not None and self.compute is None:
+            for d in changed:
+                self._exec(d, self._rank_r)
+        return changed
+
     # ------------------------------------------------------------ accounting
     def local_nnz(self, d) -> int:
         if self.erange[d] is not None:

@@ -83,6 +83,21 @@ def _worker(rank, world, port, q):
                                               strategy=strategy)
             for o, e in zip(outs, expect):
                 assert np.array_equal(o.numpy(), e), name
+            if sched in ("dynamic", "contiguous"):
+                # rebalancing from measured per-GPU times: rank 0 "ran" 3x slower,
+                # so it sheds nonzeros; the outputs stay exact
+                before = [sum(plans[d].shards[j].nnz for j in runner.assignment[d][0]) for d in range(len(plans))]
+                secs = [[3.0 * max(b, 1) for b in before],
+                        [float(max(sum(plans[d].shards[j].nnz for j in runner.assignment[d][1]), 1))
+                         for d in range(len(plans))]]
+                changed = runner.rebalance(rank_seconds=secs)
+                after = [sum(plans[d].shards[j].nnz for j in runner.assignment[d][0]) for d in range(len(plans))]
+                assert changed and all(a_ <= b_ for a_, b_ in zip(after, before)) and sum(after) < sum(before)
+                for d, p in enumerate(plans):
+                    assert rows_cover(runner.ownership[d], p.shape[d])
+                outs = runner.run([torch.from_numpy(f.copy()) for f in facs0])
+                for o, e in zip(outs, expect):
+                    assert np.array_equal(o.numpy(), e), (name, "rebalanced")
         # ragged all-gather with a ledger: every rank ends with every row
         rows = 23
         own = [[(0, 5), (9, 14)], [(5, 9), (14, 23)]]

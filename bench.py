@@ -101,6 +101,29 @@ def pcie_h2d_gbs(dev, nbytes=1 << 31):
     return best
 
 
+def plan_balance(plans):
+    """Max shard share and max row share of the nonzeros per mode (SURVEY.md
+    §8(d): the load-balance bound a single row / shard puts on N GPUs)."""
+    import torch
+
+    from paper_2507_15121_b200 import _lib
+
+    out = {"max_shard_share": [], "max_row_share": []}
+    for p in plans:
+        sizes = getattr(p, "global_shard_nnz", None)
+        sizes = np.asarray(sizes if sizes is not None else [s.nnz for s in p.shards], dtype=np.float64)
+        out["max_shard_share"].append(float(sizes.max() / max(sizes.sum(), 1)))
+        rows = p.coords[p.mode]
+        if rows is None or not rows.is_cuda:
+            out["max_row_share"].append(None)
+            continue
+        cnt = torch.empty(p.shape[p.mode], dtype=torch.int64, device=rows.device)
+        _lib.call("skrp_histogram", rows.data_ptr(), rows.numel(), cnt.numel(), cnt.data_ptr(),
+                  torch.cuda.current_stream(rows.device).cuda_stream)
+        out["max_row_share"].append(float(cnt.max().item()) / max(rows.numel(), 1))
+    return out
+
+
 def lookup_traffic(config, kernel):
     """DRAM read+write bytes per launch of `kernel` on `config` from one ncu
     --set full capture (profiles/ncu_traffic.json), or None."""
@@ -399,6 +422,12 @@ def run_ours(args, cfg):
     peak, peak_src = load_peaks()
     alg = [runner.algorithmic_bytes(i) for i in range(len(modes))]
     achieved = sum(alg) / sum(kern) / 1e9
+    # secondary roofline: compulsory bytes -- stream once,
+    # every factor read once, output written once
+    comp = [runner.local_nnz(i) * (4 * len(shape) + 4)
+            + sum(shape[w] * R * 4 for w in range(len(shape)) if w != plans[i].mode)
+            + runner.owned_rows(i) * R * 4 for i in range(len(modes))]
+    balance = plan_balance(plans)
     kernel_name = "mttkrp_panel_kernel" if plans[0].layout == "panel" else "mttkrp_v2_kernel"
     traffic = lookup_traffic(args.config, kernel_name) if world == 1 else None
 
@@ -470,7 +499,9 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": kernel_name, "kernel_ms_per_mode": [k * 1e3 for k in kern],
-                         "algorithmic_bytes_per_mode": alg},
+                         "algorithmic_bytes_per_mode": alg, "compulsory_bytes_per_mode": comp,
+                         "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak},
+            "balance": balance,
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": launches,

@@ -535,26 +535,37 @@ def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
     import dataclasses
 
     plcfg = dataclasses.replace(pl, devices=n)
-    per_rank = []
-    for r in range(n):
-        runner = DistributedMttkrp(plans, plcfg, rank=r, world=n, device=dev)
-        runner.prepare(R)
-        for _ in range(args.warmup):
-            runner.run(dev_f, exchange=False)
-        kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in modes]
-               for _ in range(args.steps)]
-        for k in range(args.steps):
-            runner.run(dev_f, kernel_events=kev[k], exchange=False)
-        torch.cuda.synchronize()
-        per_mode = [sum(kev[k][i][0].elapsed_time(kev[k][i][1]) for k in range(args.steps)) / args.steps
-                    for i in range(len(modes))]
-        per_rank.append(per_mode)
-        del runner
+
+    def time_ranks(rank_seconds=None):
+        per_rank = []
+        for r in range(n):
+            runner = DistributedMttkrp(plans, plcfg, rank=r, world=n, device=dev)
+            runner.prepare(R)
+            if rank_seconds is not None:
+                runner.rebalance(rank_seconds=rank_seconds)
+            for _ in range(args.warmup):
+                runner.run(dev_f, exchange=False)
+            kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in modes]
+                   for _ in range(args.steps)]
+            for k in range(args.steps):
+                runner.run(dev_f, kernel_events=kev[k], exchange=False)
+            torch.cuda.synchronize()
+            per_rank.append([sum(kev[k][i][0].elapsed_time(kev[k][i][1]) for k in range(args.steps)) / args.steps
+                             for i in range(len(modes))])
+            del runner
+        return per_rank
+
+    per_rank = time_ranks()
+    before = None
+    if args.rebalance:  # re-place from the measured per-rank times, then time again
+        before = per_rank
+        per_rank = time_ranks([[t / 1e3 for t in pr] for pr in per_rank])
     gather_ms = [(n - 1) / n * shape[d] * R * 4 / (link_gbs * 1e9) * 1e3 for d in modes]
     step_ms = sum(max(pr[i] for pr in per_rank) + gather_ms[i] for i in range(len(modes)))
     line = {"kind": "emulated", "metric": METRIC, "n_gpus_emulated": n, "unit": "nnz/s",
             "value_projected": len(modes) * cfg["nnz"] / (step_ms / 1e3), "ms_per_step_projected": step_ms,
             "per_rank_kernel_ms_per_mode": per_rank, "allgather_ms_per_mode_modelled": gather_ms,
+            "per_rank_kernel_ms_before_rebalance": before,
             "link_gbs_assumed": link_gbs,
             "config": {"workload": cfg["desc"], "partition": f"{cfg['strategy']}, devices={n}, oversub 4",
                        "scheduling": args.scheduling, "accumulation": args.accumulation,

@@ -264,6 +264,7 @@ class DistributedMttkrp:
         rank_r = factors[0].shape[1]
         if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
             self.prepare(rank_r, factors[0].dtype)
+        self._exchange = exchange
         facs = list(factors)
         for d, plan in enumerate(self.plans):
             out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
@@ -311,7 +312,7 @@ class DistributedMttkrp:
                        peers=self._peers[d])
             else:
                 ex.run(coords, vals, plan.nnz, plan.mode, factors, out, self.cfg, stream.cuda_stream, events=events)
-        if self.boundary[d]:
+        if self.boundary[d] and getattr(self, "_exchange", True):
             self._reduce_boundary(d, out)
         return out
 

@@ -484,21 +484,44 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                     run[q] = (c < RR) ? carry_row[c] : 0.f;
                 }
                 uint32_t row = cur;
-                for (int e = 0; e < nin; ++e) {
-                    if ((cm >> e) & 1u) {
-                        float *pr = prow(row);
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) {
-                            const int c = lane + 32 * q;
-                            if (c < RR) pr[c] += run[q];
-                            run[q] = 0.f;
-                        }
-                        row = __shfl_sync(kFull, r_l, e);
-                    }
+                auto flush_cols = [&](uint32_t rw) {
+                    float *pr = prow(rw);
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) {
                         const int c = lane + 32 * q;
-                        if (c < RR) run[q] += stage[e * STR + c];
+                        if (c < RR) pr[c] += run[q];
+                        run[q] = 0.f;
+                    }
+                };
+                if constexpr (CPL <= 2) {
+                    // staged values first (pipelined LDS), then an FADD-chain fold
+                    float sv[CPL][32];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = lane + 32 * q;
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) sv[q][e] = (c < RR && e < nin) ? stage[e * STR + c] : 0.f;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        if ((cm >> e) & 1u) {
+                            flush_cols(row);
+                            row = __shfl_sync(kFull, r_l, e);
+                        }
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) run[q] += sv[q][e];
+                    }
+                } else {
+                    for (int e = 0; e < nin; ++e) {
+                        if ((cm >> e) & 1u) {
+                            flush_cols(row);
+                            row = __shfl_sync(kFull, r_l, e);
+                        }
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) {
+                            const int c = lane + 32 * q;
+                            if (c < RR) run[q] += stage[e * STR + c];
+                        }
                     }
                 }
 #pragma unroll

@@ -318,18 +318,43 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             // the open row: cur continued by nonzero 0, or the row nonzero 0 opens
             uint32_t row = cur;  // nonzero 0 continues cur (a closed cur was written above)
             bool rhead = head;   // tile head only while the first row is open
-            for (int e = 0; e < nin; ++e) {
-                if ((cm >> e) & 1u) {
-                    write_cols(row, run, rhead);
-                    rhead = false;
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) run[q] = 0.f;
-                    row = __shfl_sync(kFull, r_l, e);
-                }
+            if constexpr (CPL <= 2) {
+                // all staged values first (independent LDS, pipelined), then the
+                // fold: an FADD chain instead of an LDS->FADD chain per nonzero
+                // (short runs made that chain the kernel's critical path)
+                float sv[CPL][32];
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) {
                     const int c = lane + 32 * q;
-                    if (c < RR) run[q] += stage[e * STR + c];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) sv[q][e] = (c < RR && e < nin) ? stage[e * STR + c] : 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    if ((cm >> e) & 1u) {
+                        write_cols(row, run, rhead);
+                        rhead = false;
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) run[q] = 0.f;
+                        row = __shfl_sync(kFull, r_l, e);
+                    }
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) run[q] += sv[q][e];
+                }
+            } else {
+                for (int e = 0; e < nin; ++e) {
+                    if ((cm >> e) & 1u) {
+                        write_cols(row, run, rhead);
+                        rhead = false;
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) run[q] = 0.f;
+                        row = __shfl_sync(kFull, r_l, e);
+                    }
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = lane + 32 * q;
+                        if (c < RR) run[q] += stage[e * STR + c];
+                    }
                 }
             }
             // the last row stays open: back to the register layout (slot 0)

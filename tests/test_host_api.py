@@ -376,3 +376,22 @@ def test_plan_cache_rejects_non_plan_files(tmp_path):
     p.write_bytes(b"definitely not a plan")
     with pytest.raises(sk.PlanVersionError, match="not a plan cache file"):
         sk.load_plan(p)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the reference algorithm on the host cores):
+    one JSON line with the contract's keys, cpu_baseline and an e2e object
+    that moves no bytes across the host link."""
+    import json
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["unit"] == "nnz/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0

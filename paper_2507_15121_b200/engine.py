@@ -319,6 +319,31 @@ def _skewed_rows(plan, shard_ids=None, warps=16) -> bool:
     return int(counts.max().item()) * 4 * sms * warps > nnz
 
 
+def streamed_blocking(plan, rank, block_mb=32, stream_mb=256):
+    """'Pin one, stream one' block shapes (measured best on cfg2 for every
+    mode, profiles/sweeps/r01d_sweep_o.jsonl: 48.3/49.0/49.1 ms vs 52.5/51.7/
+    51.5 for the cost model's two-block shapes): the smallest input factor
+    larger than one block but at most `stream_mb` streams through L2
+    unblocked, every other large input is cut into `block_mb` blocks that stay
+    L2-resident while a group runs; few groups keep the output re-sweeps and
+    the runs short-run free.  None when no input qualifies."""
+    n, d = len(plan.shape), plan.mode
+    row_b = rank * 4
+    big = [w for w in range(n) if w != d and plan.shape[w] * row_b > (block_mb << 20)]
+    if not big:
+        return None
+    cand = [w for w in big if plan.shape[w] * row_b <= (stream_mb << 20)]
+    if not cand:
+        return None
+    stream = min(cand, key=lambda w: plan.shape[w])
+    shifts = [-1] * n
+    rows = max(1, (block_mb << 20) // row_b)
+    for w in big:
+        if w != stream:
+            shifts[w] = max(0, rows.bit_length() - 1)
+    return shifts if any(x >= 0 for x in shifts) else None
+
+
 def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
@@ -333,11 +358,21 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
         if cfg.layout == "blocked":
             raise ValueError("blocked layout needs R in {8,16,32,64,128} and N <= 5")
         return plan
-    if cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce" and _skewed_rows(plan, shard_ids):
+    skewed = _skewed_rows(plan, shard_ids)
+    if cfg.layout == "auto" and cfg.accumulation == "deterministic-reduce" and skewed:
         # skewed rows under deterministic-reduce: plan order + carry tree runs at
         # the atomic speed (cfg4s 28.4 vs 29.2 ms/step, cfg5s 56.6 vs 56.7),
         # the blocked carry path pays per-group launches (123 / 191 ms)
         return plan
+    if cfg.layout == "auto" and not skewed and len(plan.shape) == 3:
+        sh = streamed_blocking(plan, rank)
+        if sh is not None:
+            if cfg.accumulation == "deterministic-reduce" and panel_shape(len(plan.shape), rank) is not None:
+                prm = choose_panels(plan, rank, cfg, shard_ids)
+                plan.to_panels(prm[0], sh, prm[2])
+            else:
+                plan.to_blocked(sh)
+            return plan
     shifts, cost, base = choose_blocking(plan, rank, shard_ids, cfg.l2_budget_mb << 20,
                                          max_blocks=cfg.max_blocks, force=cfg.layout == "blocked")
     if shifts is not None and (cfg.layout == "blocked" or cost < 0.8 * base):

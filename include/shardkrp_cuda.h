@@ -66,6 +66,13 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
                                     accumulation the caller launches one block
                                     group at a time and flushes read-add-write */
 
+#define SKRP_FLAG_STREAM_INPUT0 2 /* input 0 (the first mode != mode, ascending) is
+                                    an unblocked STREAMED factor next to pinned
+                                    blocks of the other input: its rows are
+                                    loaded L2::evict_first so they do not push
+                                    the pinned block out (R = 32, N = 3) */
+#define SKRP_FLAG_STREAM_INPUT1 4 /* same for input 1 */
+
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
 int skrp_abi_version(void);  /* 4: panel peer-output push, IPC entry points */

@@ -21,6 +21,8 @@ SKRP_OK, SKRP_ERR_INVALID, SKRP_ERR_CUDA, SKRP_ERR_NOMEM, SKRP_ERR_NONFINITE = 0
 SKRP_MAX_MODES = 8
 ACC_DETERMINISTIC, ACC_ATOMIC = 0, 1
 FLAG_ADDITIVE = 1
+FLAG_STREAM_INPUT0 = 2
+FLAG_STREAM_INPUT1 = 4
 PANEL_LOCKSTEP = 1
 
 vp = ctypes.c_void_p

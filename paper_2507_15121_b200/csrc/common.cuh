@@ -128,6 +128,15 @@ __device__ __forceinline__ void prefetch_l2_last(const void *p)
     asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
 }
 
+// evict_first factor row (a streamed, unblocked input must not displace the
+// pinned block of the other input)
+__device__ __forceinline__ void ld_row8_first(float (&v)[8], const float *p)
+{
+    asm("ld.global.nc.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
+
 // no eviction hint (A/B of the L2 policy)
 __device__ __forceinline__ void ld_row8_plain(float (&v)[8], const float *p)
 {

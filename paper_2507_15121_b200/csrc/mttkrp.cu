@@ -430,6 +430,12 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 11 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 0>();  // output: no hint
         if (a.variant == 12 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1, 0>();  // no factor/output hints
         if (a.variant == 13 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 0>();  // 24 warps/SM, output normal
+        // streamed-input load policy (pin-one-stream-one shapes): input 0 / 1
+        // loaded without the evict_last hint (19/20) or with evict_first (21/22)
+        if (a.variant == 19 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 2>();
+        if (a.variant == 20 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 4>();
+        if (a.variant == 21 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 10>();
+        if (a.variant == 22 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 12>();
         // L2 prefetch of the next batch's rows (A/B)
         if (a.variant == 17 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 1, 1>();
         if (a.variant == 18 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 1, 1>();
@@ -440,6 +446,11 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 9 && a.rank == 64) {
             if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
             if (a.nmodes == 4) return mk2<4, 8, 4, 1>();
+        }
+        if (a.variant == 0 && a.nmodes == 3 && a.rank == 32) {
+            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 12>();
         }
         if (a.variant == 0) {
             if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;
@@ -467,15 +478,20 @@ struct PanelVariant {
     size_t stage = 0;
 };
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0>
 static PanelVariant mkp()
 {
-    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF>, NW, 8 * LPN,
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF, SM>, NW, 8 * LPN,
                         panel_stage_bytes<8 * LPN, NW, ALG>()};
 }
 
-static PanelVariant choose_panel(int nmodes, int rank, int variant = 0)
+static PanelVariant choose_panel(int nmodes, int rank, int variant = 0, int flags = 0)
 {
+    if (nmodes == 3 && rank == 32 && variant == 0) {  // streamed input: evict_first loads
+        const int sm = flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+        if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 0, 0, 0, 1>();
+        if (sm == SKRP_FLAG_STREAM_INPUT1) return mkp<3, 4, 4, 16, 0, 0, 0, 2>();
+    }
     // A/B variants (R = 32, N = 3): 1 = gathers without L1 allocation,
     // 2 = 8 warps per CTA, 3 = both
     if (nmodes == 3 && rank == 32 && variant == 1) return mkp<3, 4, 4, 16, 1>();
@@ -594,7 +610,7 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
     SKRP_REQUIRE(a.mode >= 0 && a.mode < a.nmodes, "mode %d out of range", a.mode);
     SKRP_REQUIRE(p.num_items >= 0 && p.groups >= 1, "bad item count / groups");
     if (p.num_items == 0) return SKRP_OK;
-    PanelVariant v = choose_panel(a.nmodes, a.rank, a.variant);
+    PanelVariant v = choose_panel(a.nmodes, a.rank, a.variant, a.flags);
     SKRP_REQUIRE(v.fn != nullptr, "no panel kernel for nmodes=%d rank=%d", a.nmodes, a.rank);
     SKRP_REQUIRE(p.warps == v.warps, "panel layout built for %d warps, kernel uses %d", p.warps, v.warps);
     SKRP_REQUIRE(p.slab_rows >= p.warps && (p.slab_rows & (p.slab_rows - 1)) == 0 && p.slab_rows <= panel_max_slab(v),

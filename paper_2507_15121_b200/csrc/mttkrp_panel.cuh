@@ -47,7 +47,7 @@ __device__ __forceinline__ void grid_wait(unsigned long long *counter, unsigned 
     }
 }
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0>
 __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     mttkrp_panel_kernel(const skrp_mttkrp_args a, const skrp_panel_args pa)
 {
@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                         for (int j = 0; j < NIN; ++j) {
                             const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
                             if constexpr (L1NA) ld_row8_na(gv[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                            else if ((SM >> j) & 1) ld_row8_first(gv[u][j], F[j] + (size_t)idx * fld + col);
                             else ld_row<VEC>(gv[u][j], F[j] + (size_t)idx * fld + col, 0);
                         }
                     }

@@ -248,7 +248,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                        if constexpr (PLAIN) ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                        // PLAIN: 1 = no L2 hint on every input; bits 1/2 (+4) mark
+                        // input 0/1 as streamed (evict_first 4-bit variants) so it
+                        // does not displace the pinned block of the other input
+                        if constexpr (PLAIN == 1) ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                        else if constexpr (PLAIN >= 2) {
+                            if ((PLAIN >> (j + 1)) & 1) {
+                                if constexpr (PLAIN & 8) ld_row8_first(g[u][j], F[j] + (size_t)idx * fld + col);
+                                else ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                            } else {
+                                ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                            }
+                        }
                         else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
                     }
                 }

@@ -422,7 +422,7 @@ class _ShardExec:
         self.blocked = plan.layout == "blocked"
         if clip is not None and self.blocked:
             raise ValueError("element-split placement needs the plan-order (flycoo) layout")
-        self.flags = _lib.FLAG_ADDITIVE if self.blocked else 0
+        self.flags = (_lib.FLAG_ADDITIVE if self.blocked else 0) | _stream_flags(plan, rank)
         self.nnz = (int(clip[1] - clip[0]) if clip is not None
                     else int(sum(plan.shards[j].nnz for j in shard_ids)))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
@@ -554,6 +554,24 @@ class _ShardExec:
             events[1].record()
 
 
+def _stream_flags(plan, rank) -> int:
+    """SKRP_FLAG_STREAM_INPUTj for a pin-one-stream-one layout (one large input
+    left unblocked next to a blocked one): that input's rows are loaded
+    L2::evict_first so they do not push the pinned blocks out (cfg2: 48.1 ->
+    46.2, 49.5 -> 47.3, 49.2 -> 46.8 ms per mode; profiles/sweeps/r01d_sweep_p.jsonl)."""
+    sh = getattr(plan, "block_shifts", None)
+    if sh is None or plan.layout not in ("blocked", "panel") or len(plan.shape) != 3 or rank != 32:
+        return 0
+    ins = [w for w in range(3) if w != plan.mode]
+    if not any(sh[w] >= 0 for w in ins):
+        return 0
+    flags = 0
+    for j, w in enumerate(ins):
+        if sh[w] < 0 and plan.shape[w] * rank * 4 > (32 << 20):
+            flags |= 2 << j
+    return flags if flags in (_lib.FLAG_STREAM_INPUT0, _lib.FLAG_STREAM_INPUT1) else 0
+
+
 class _StreamExec:
     """Out-of-core executor: the plan lives in pinned
     host memory (plan.to_host()); each run copies it to two device buffers
@@ -680,6 +698,7 @@ class _PanelExec:
         self.groups = pn["groups"]
         self.warps = pn["warps"]
         self.slab_rows = 1 << pn["slab_shift"]
+        self.stream_flags = _stream_flags(plan, rank)
         self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
         # grid-synchronised rounds only pay when items are about equal
         # (uniform tensors); skewed items are claimed dynamically
@@ -710,6 +729,7 @@ class _PanelExec:
         a.out = out.data_ptr()
         a.work_counter = self.counter.data_ptr()
         a.variant = cfg.kernel_variant
+        a.flags = self.stream_flags
         pa = _lib.PanelArgs()
         pa.item_rows = self.item_rows.data_ptr()
         pa.item_offsets = self.item_offsets.data_ptr()

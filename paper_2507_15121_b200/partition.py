@@ -335,7 +335,7 @@ class ModePartitionPlan:
         self.exec_perm = perm if self.perm is not None else None
         return sorted_keys
 
-    def to_panels(self, slab_shift, shifts, warps, order=None):
+    def to_panels(self, slab_shift, shifts, warps, order=None, sweep=None):
         """Reorder the device arrays IN PLACE into the PANEL execution layout
         of the output-stationary kernel (csrc/mttkrp_panel.cuh): key =
         [shard | slab (c_d >> slab_shift) | input blocks (c_w >> shifts[w], in
@@ -363,10 +363,16 @@ class ModePartitionPlan:
         in_w = [max(1, _key_bits(-(-self.shape[w] // (1 << shifts[w])))) for w in order]
         parts = ([(self.coords[d], slab_shift, slab_w)] + [(self.coords[w], shifts[w], b) for w, b in zip(order, in_w)]
                  + ([(self.coords[d], stripe_shift, stripe_bits)] if stripe_bits else []))
+        # sweep = {mode: shift}: sub-blocks sorted INSIDE every (group, stripe)
+        # range, so all CTAs walk that input in ascending order together
+        sweep = dict(sweep or {})
+        sweep_w = [max(1, _key_bits(-(-self.shape[w] // (1 << sft)))) for w, sft in sweep.items()]
+        parts += [(self.coords[w], sft, b) for (w, sft), b in zip(sweep.items(), sweep_w)]
+        sweep_bits = sum(sweep_w)
         k = self.shard_count
         shard_bits = max(1, _key_bits(k))
         group_bits = sum(in_w)
-        total_bits = shard_bits + slab_w + group_bits + stripe_bits
+        total_bits = shard_bits + slab_w + group_bits + stripe_bits + sweep_bits
         if total_bits > 31:
             raise ValueError(f"panel key needs {total_bits} > 31 bits (use larger slabs or blocks)")
         dev = self.vals.device
@@ -379,18 +385,19 @@ class ModePartitionPlan:
                 continue
             for s_ in range(lo >> slab_shift, ((hi - 1) >> slab_shift) + 1):
                 rows.append((max(lo, s_ << slab_shift), min(hi, (s_ + 1) << slab_shift)))
-                bases.append(((j << slab_w) | s_) << (group_bits + stripe_bits))
+                bases.append(((j << slab_w) | s_) << (group_bits + stripe_bits + sweep_bits))
         groups = 1 << group_bits
         per = groups * warps
         base = torch.tensor(bases, dtype=torch.int64, device=dev)
-        q = (base[:, None] + torch.arange(per + 1, dtype=torch.int64, device=dev)[None, :])
-        q[:, per] = base + (1 << (group_bits + stripe_bits))  # end of the item = start of the next slab key
+        q = (base[:, None] + (torch.arange(per + 1, dtype=torch.int64, device=dev)[None, :] << sweep_bits))
+        q[:, per] = base + (1 << (group_bits + stripe_bits + sweep_bits))  # end = the next slab's first key
         offs = torch.searchsorted(sorted_keys, q.to(torch.int32).reshape(-1)).reshape(len(bases), per + 1)
         del sorted_keys
         self.panel = {
             "slab_shift": slab_shift, "warps": warps, "groups": groups, "order": order,
             "item_rows": np.asarray(rows, dtype=np.int64).reshape(-1, 2),
-            "item_shard": np.asarray([b >> (group_bits + stripe_bits + slab_w) for b in bases], dtype=np.int64),
+            "item_shard": np.asarray([b >> (group_bits + stripe_bits + sweep_bits + slab_w) for b in bases],
+                                     dtype=np.int64),
             "item_offsets": offs.to(torch.int64).contiguous(),
         }
         self.groups = None

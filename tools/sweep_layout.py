@@ -54,7 +54,8 @@ def main():
         d = sp["mode"]
         got = ctypes.c_int64()
         _lib.call("skrp_set_l2_persisting", int(sp.get("persist_mb", 0)) << 20, ctypes.byref(got))
-        key = (d, sp.get("layout"), sp.get("slab_shift"), tuple(sp.get("shifts") or []), tuple(sp.get("order") or []))
+        key = (d, sp.get("layout"), sp.get("slab_shift"), tuple(sp.get("shifts") or []), tuple(sp.get("order") or []),
+               json.dumps(sp.get("sweep")), sp.get("warps"))
         if key != cache_key:
             plan = None
             gc.collect()  # plans and their shards reference each other
@@ -63,7 +64,8 @@ def main():
             t0 = time.perf_counter()
             if sp.get("layout") == "panel":
                 warps = sp.get("warps") or panel_shape(len(shape), R // sp.get("passes", 1))[0]
-                plan.to_panels(sp["slab_shift"], sp["shifts"], warps, sp.get("order"))
+                plan.to_panels(sp["slab_shift"], sp["shifts"], warps, sp.get("order"),
+                               sweep={int(k): v for k, v in (sp.get("sweep") or {}).items()})
             elif sp.get("shifts"):
                 plan.to_blocked(sp["shifts"], sp.get("order"))
             block_s = time.perf_counter() - t0

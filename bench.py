@@ -369,7 +369,10 @@ def run_ours(args, cfg):
 
     for _ in range(args.warmup):
         runner.run(dev_f)
-    rebalanced = runner.rebalance(dev_f) if args.rebalance and world > 1 else []
+    rebalanced = []
+    if args.rebalance and world > 1:
+        for _ in range(args.rebalance_rounds):
+            rebalanced = sorted(set(rebalanced) | set(runner.rebalance(dev_f)))
     barrier()
 
     # ---- timed region: K all-mode steps, inputs resident in HBM
@@ -536,12 +539,12 @@ def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
 
     plcfg = dataclasses.replace(pl, devices=n)
 
-    def time_ranks(rank_seconds=None):
+    def time_ranks(history=None):
         per_rank = []
         for r in range(n):
             runner = DistributedMttkrp(plans, plcfg, rank=r, world=n, device=dev)
             runner.prepare(R)
-            if rank_seconds is not None:
+            for rank_seconds in history or []:  # replay the rebalancing rounds
                 runner.rebalance(rank_seconds=rank_seconds)
             for _ in range(args.warmup):
                 runner.run(dev_f, exchange=False)
@@ -557,9 +560,12 @@ def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
 
     per_rank = time_ranks()
     before = None
-    if args.rebalance:  # re-place from the measured per-rank times, then time again
+    if args.rebalance:  # re-place from the measured per-rank times, then time again (rounds)
         before = per_rank
-        per_rank = time_ranks([[t / 1e3 for t in pr] for pr in per_rank])
+        history = []
+        for _ in range(args.rebalance_rounds):
+            history.append([[t / 1e3 for t in pr] for pr in per_rank])
+            per_rank = time_ranks(history)
     gather_ms = [(n - 1) / n * shape[d] * R * 4 / (link_gbs * 1e9) * 1e3 for d in modes]
     step_ms = sum(max(pr[i] for pr in per_rank) + gather_ms[i] for i in range(len(modes)))
     line = {"kind": "emulated", "metric": METRIC, "n_gpus_emulated": n, "unit": "nnz/s",
@@ -752,6 +758,7 @@ def main():
                                                       "memory ('all' or e.g. '0,2'; atomic accumulation)")
     ap.add_argument("--rebalance", action="store_true",
                     help="N>1: re-place shards from measured per-GPU kernel times after the warm-up")
+    ap.add_argument("--rebalance-rounds", type=int, default=2, help="measure + re-place rounds for --rebalance")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",

@@ -62,38 +62,47 @@ class DistributedMttkrp:
         self.erange = [None] * len(self.plans)   # element range (split placement)
         self.boundary = [[] for _ in self.plans]  # rows summed across ranks (split)
         self.touch = [None] * len(self.plans)    # rows this rank writes (split)
+        self._cuts = [None] * len(self.plans)
         if cfg.scheduling == "split":
-            for d, p in enumerate(self.plans):
-                info = getattr(p, "split_info", None)
-                if info is not None:  # split-routed distributed plan: local = my element range
-                    bnd, rcut = info["boundary"], info["rcut"]
-                    self.erange[d] = (0, p.nnz)
-                    self.mine[d] = [s_.shard_id for s_ in p.shards if s_.nnz]
-                else:
-                    ranges, ids, bnd, rcut = assign_elements(p, self.world)
-                    self.erange[d] = ranges[self.rank]
-                    self.mine[d] = ids[self.rank]
-                self.boundary[d] = bnd
-                bset = set(bnd)
-                own = []
-                for r in range(self.world):
-                    lo, hi = rcut[r], rcut[r + 1]
-                    rr, cur = [], lo
-                    for b in bnd:  # boundary rows are all-reduced, not broadcast
-                        if lo <= b < hi:
-                            if b > cur:
-                                rr.append((cur, b))
-                            cur = b + 1
-                    if hi > cur:
-                        rr.append((cur, hi))
-                    own.append(rr)
-                self.ownership[d] = own
-                lo, hi = rcut[self.rank], rcut[self.rank + 1]
-                if hi in bset:
-                    hi += 1
-                self.touch[d] = (lo, min(hi, p.shape[p.mode]))
+            for d in range(len(self.plans)):
+                self._set_split(d)
         self._execs = {}
         self.outputs = None
+
+    def _set_split(self, d, cuts=None):
+        """Element-split placement of mode d (cut positions in plan order;
+        default equal nonzeros): element range, shards, boundary rows summed
+        across ranks, owned row ranges, rows this rank writes."""
+        p = self.plans[d]
+        info = getattr(p, "split_info", None)
+        if info is not None:  # split-routed distributed plan: local = my element range
+            bnd, rcut = info["boundary"], info["rcut"]
+            self.erange[d] = (0, p.nnz)
+            self.mine[d] = [s_.shard_id for s_ in p.shards if s_.nnz]
+        else:
+            ranges, ids, bnd, rcut = assign_elements(p, self.world, cuts=cuts)
+            self._cuts[d] = [r[0] for r in ranges] + [ranges[-1][1]]
+            self.erange[d] = ranges[self.rank]
+            self.mine[d] = ids[self.rank]
+        self.boundary[d] = bnd
+        bset = set(bnd)
+        own = []
+        for r in range(self.world):
+            lo, hi = rcut[r], rcut[r + 1]
+            rr, cur = [], lo
+            for b in bnd:  # boundary rows are all-reduced, not broadcast
+                if lo <= b < hi:
+                    if b > cur:
+                        rr.append((cur, b))
+                    cur = b + 1
+            if hi > cur:
+                rr.append((cur, hi))
+            own.append(rr)
+        self.ownership[d] = own
+        lo, hi = rcut[self.rank], rcut[self.rank + 1]
+        if hi in bset:
+            hi += 1
+        self.touch[d] = (lo, min(hi, p.shape[p.mode]))
 
     # ----------------------------------------------------------- rebalancing
     def measure_mode_seconds(self, factors, chained=True):
@@ -127,6 +136,30 @@ class DistributedMttkrp:
             rank_seconds = allt
         changed = []
         for d, p in enumerate(self.plans):
+            if self.cfg.scheduling == "split" and self._cuts[d] is not None:
+                # cost-weighted element cuts: per-element cost is piecewise
+                # constant (each rank's measured time / its elements); cut the
+                # cumulative cost into equal parts
+                cuts = self._cuts[d]
+                t = np.array([rank_seconds[r][d] for r in range(self.world)], dtype=np.float64)
+                n_r = np.diff(np.asarray(cuts, dtype=np.float64))
+                if not np.all(t > 0):
+                    continue
+                cum = np.concatenate([[0.0], np.cumsum(t)])
+                new = [0]
+                for j in range(1, self.world):
+                    target = j * cum[-1] / self.world
+                    r = int(np.searchsorted(cum, target, side="right") - 1)
+                    r = min(max(r, 0), self.world - 1)
+                    pos = cuts[r] + (target - cum[r]) / t[r] * n_r[r] if t[r] > 0 else cuts[r]
+                    new.append(int(min(max(round(pos), new[-1]), p.nnz)))
+                new.append(p.nnz)
+                if new != list(cuts):
+                    self._set_split(d, new)
+                    for key in [k for k in self._execs if k[0] == d]:
+                        del self._execs[key]
+                    changed.append(d)
+                continue
             if self.cfg.scheduling not in ("contiguous", "dynamic") or getattr(p, "global_shard_nnz", None) is not None:
                 continue
             owner = np.empty(p.shard_count, dtype=np.int64)

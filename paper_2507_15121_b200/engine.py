@@ -162,13 +162,14 @@ def elementwise_compute(x: NonzeroElement, factors, mode: int):
 # ----------------------------------------------------------------- balancer
 
 
-def assign_elements(plan: ModePartitionPlan, m: int):
+def assign_elements(plan: ModePartitionPlan, m: int, cuts=None):
     """Element-split placement: device r processes plan elements
-    [r*n//m, (r+1)*n//m) (plan order).  Returns (ranges, shard ids per device,
-    boundary rows cut by a range edge, row cuts R_0..R_m)."""
+    [cuts[r], cuts[r+1]) (plan order; default r*n//m, equal nonzeros).
+    Returns (ranges, shard ids per device, boundary rows cut by a range edge,
+    row cuts R_0..R_m)."""
     torch = _torch()
     n = plan.nnz
-    cuts = [r * n // m for r in range(m + 1)]
+    cuts = [r * n // m for r in range(m + 1)] if cuts is None else [int(c) for c in cuts]
     rowc = plan.coords[plan.mode]
     probe = sorted({c for c in cuts if 0 < c < n} | {c - 1 for c in cuts if 0 < c < n})
     val = {}

@@ -894,3 +894,34 @@ def test_plan_cache_reference_files(golden, tmp_path):
     bad.write_bytes(bytes(v2))
     with pytest.raises(sk.PlanVersionError, match="plan version 2"):
         sk.load_plan(bad)
+
+
+@pytest.mark.parametrize("layout", ["blocked", "panel"])
+def test_streamed_input_policy_parity(layout):
+    """Pin-one-stream-one layouts with factors > 32 MB: the streamed input is
+    flagged (SKRP_FLAG_STREAM_INPUTj -> evict_first loads) in the tile and
+    panel kernels; every mode matches the oracle."""
+    from paper_2507_15121_b200.engine import _stream_flags, panel_shape, streamed_blocking
+
+    shape = (2000, 300_000, 280_000)
+    t = sk.synth_tensor_device(shape, 1_500_000, seed=12)
+    fs = sk.random_factors(shape, 32, seed=5)
+    facs = [f.data for f in fs]
+    idx, vals = t.indices, t.values
+    for d in range(3):
+        p = sk.build_mode_plan(t, d, sk.PartitionConfig())
+        sh = streamed_blocking(p, 32)
+        if sh is None:  # mode 0's inputs are both > 32 MB; modes 1/2 have a small input
+            sh = [-1 if w == d else (17 if w == max(w_ for w_ in range(3) if w_ != d) else -1) for w in range(3)]
+        if layout == "panel":
+            warps, _ = panel_shape(3, 32)
+            p.to_panels(9, sh, warps)
+        else:
+            p.to_blocked(sh)
+        flags = _stream_flags(p, 32)
+        cfg = sk.PlatformConfig(rank=32, accumulation="atomic")
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+        expect = oracle.mttkrp_seq_c(idx, vals, facs, d)
+        assert rel_err(out, expect) <= TOL, (layout, d, flags)
+        if d == 0:
+            assert flags in (_lib.FLAG_STREAM_INPUT0, _lib.FLAG_STREAM_INPUT1)

@@ -503,7 +503,11 @@ def run_ours(args, cfg):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": kernel_name, "kernel_ms_per_mode": [k * 1e3 for k in kern],
                          "algorithmic_bytes_per_mode": alg, "compulsory_bytes_per_mode": comp,
-                         "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak},
+                         "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak,
+                         # measured DRAM bytes of the mode-0 launch (ncu) over its live time: how
+                         # close the kernel runs to the HBM roofline on the bytes it really moves
+                         "dram_gbs_mode0": (traffic / kern[0] / 1e9) if traffic else None,
+                         "frac_dram_mode0": (traffic / kern[0] / 1e9 / peak) if traffic else None},
             "balance": balance,
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},

@@ -435,6 +435,11 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 19 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 2>();
         if (a.variant == 20 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 4>();
         if (a.variant == 21 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 10>();
+        if (a.variant == 24 && a.rank == 32 && a.nmodes == 3) {  // + no L1 allocation for the gathers
+            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 26>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 28>();
+        }
         if (a.variant == 23 && a.rank == 32 && a.nmodes == 3) {  // 24 warps/SM with the streamed-input policy
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 2, 3, 10>();

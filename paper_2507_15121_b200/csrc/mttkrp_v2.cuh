@@ -253,11 +253,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                         // does not displace the pinned block of the other input
                         if constexpr (PLAIN == 1) ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
                         else if constexpr (PLAIN >= 2) {
+                            // bit 4 (16): no L1 allocation for any gather
                             if ((PLAIN >> (j + 1)) & 1) {
-                                if constexpr (PLAIN & 8) ld_row8_first(g[u][j], F[j] + (size_t)idx * fld + col);
+                                if constexpr ((PLAIN & 8) && (PLAIN & 16))
+                                    ld_row8_first_na(g[u][j], F[j] + (size_t)idx * fld + col);
+                                else if constexpr (PLAIN & 8) ld_row8_first(g[u][j], F[j] + (size_t)idx * fld + col);
                                 else ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
                             } else {
-                                ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                                if constexpr (PLAIN & 16) ld_row8_last_na(g[u][j], F[j] + (size_t)idx * fld + col);
+                                else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
                             }
                         }
                         else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);

@@ -249,7 +249,6 @@ def run_reference(args, cfg):
     sample = cfg["nnz"] if cfg["nnz"] <= 5_000_000 else cfg["nnz"] // 64
     modes_shape = shape
     t_all = []
-    import oracle as orc  # noqa: F401
 
     idx, vals = host_sample(shape, sample, 1)
     fac0 = [np.random.default_rng(0).random((s, cfg["rank"])) for s in shape]

@@ -29,7 +29,7 @@ from __future__ import annotations
 import ctypes
 import time
 import warnings
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

@@ -925,3 +925,30 @@ def test_streamed_input_policy_parity(layout):
         assert rel_err(out, expect) <= TOL, (layout, d, flags)
         if d == 0:
             assert flags in (_lib.FLAG_STREAM_INPUT0, _lib.FLAG_STREAM_INPUT1)
+
+
+def test_scaling_floor_per_rank_share():
+    """SPEC acceptance 6 (scaling floor t1/t4 > 1.5), on one GPU: the kernel
+    time of the whole all-mode step vs the slowest of the 4 ranks' shares of
+    the same plans (each share timed alone, compute only -- what every GPU of
+    a 4-GPU run executes between the all-gathers)."""
+    from paper_2507_15121_b200.distributed import DistributedMttkrp
+
+    shape = (480_000, 180_000, 180_000)
+    t = sk.synth_tensor_device(shape, 40_000_000, seed=2)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4), keep_permutation=False)
+    fs = [torch.rand((s, 32), device="cuda") for s in shape]
+
+    def kernel_seconds(runner):
+        for _ in range(2):
+            runner.run(fs, exchange=False)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
+        runner.run(fs, kernel_events=ev, exchange=False)
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in ev)
+
+    cfg = sk.PlatformConfig(devices=4, rank=32, accumulation="atomic", scheduling="contiguous")
+    t1 = kernel_seconds(DistributedMttkrp(plans, sk.PlatformConfig(devices=1, rank=32, accumulation="atomic"),
+                                          rank=0, world=1))
+    t4 = max(kernel_seconds(DistributedMttkrp(plans, cfg, rank=r, world=4)) for r in range(4))
+    assert t1 / t4 > 1.5, (t1, t4)

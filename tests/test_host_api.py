@@ -395,3 +395,28 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["unit"] == "nnz/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_spec_acceptance_imbalance():
+    """SPEC acceptance 5 on the host balancer: device loads (nonzeros per
+    device under the reference's dynamic claim queue) are within 5 % on a
+    uniform tensor, and on a Zipf tensor equal-index is more imbalanced than
+    nnz-balanced (SPEC S:153 / S:481)."""
+    from types import SimpleNamespace
+
+    import oracle
+    from paper_2507_15121_b200.engine import assign_shards
+
+    def imbalance(idx, shape, strategy, m=4):
+        p = oracle.plan(idx, shape, 0, devices=m, strategy=strategy)
+        sizes = np.diff(p["offsets"])
+        fake = SimpleNamespace(shard_count=len(sizes), shards=[SimpleNamespace(nnz=int(x)) for x in sizes])
+        loads = [sum(int(sizes[j]) for j in ids) for ids in assign_shards(fake, m, "dynamic")]
+        return (max(loads) - min(loads)) / max(sum(loads), 1) * 100
+
+    rng = np.random.default_rng(1)
+    shape = (1000, 100, 100)
+    uni = np.stack([rng.integers(0, s, 200_000) for s in shape], 1)
+    assert imbalance(uni, shape, "equal-index") < 5.0
+    z = np.stack([np.minimum(rng.zipf(1.2, 200_000) - 1, s - 1) for s in shape], 1)
+    assert imbalance(z, shape, "equal-index") > imbalance(z, shape, "nnz-balanced")

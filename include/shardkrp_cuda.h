@@ -75,7 +75,7 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 4: panel peer-output push, IPC entry points */
+int skrp_abi_version(void);  /* 5: per-launch L2 access-policy window in skrp_mttkrp_args */
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200
@@ -147,6 +147,13 @@ typedef struct {
                                                 of a wider row or a column plane    */
     int32_t out_ld;                          /* floats between output rows (0 = R);
                                                 `out` may point at a column offset   */
+    const void *l2_window_base;              /* optional L2 access-policy window for
+                                                this launch (a pinned factor block):
+                                                hits persist in the set-aside L2,
+                                                misses stream; 0 bytes = none        */
+    int64_t l2_window_bytes;
+    float l2_window_hit_ratio;
+    int32_t reserved2;
 } skrp_mttkrp_args;
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);

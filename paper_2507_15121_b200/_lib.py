@@ -32,7 +32,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 4  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 5  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -56,6 +56,10 @@ class MttkrpArgs(ctypes.Structure):
         ("flags", i32),
         ("factor_ld", i32),
         ("out_ld", i32),
+        ("l2_window_base", vp),
+        ("l2_window_bytes", i64),
+        ("l2_window_hit_ratio", ctypes.c_float),
+        ("reserved2", i32),
     ]
 
 

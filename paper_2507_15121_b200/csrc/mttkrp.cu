@@ -593,10 +593,28 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
     ctas = std::min<int64_t>(ctas, (a.num_tiles + kWarpsPerCta - 1) / kWarpsPerCta);
     SKRP_CUDA(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), s));
     unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
-    if (v.v2)
+    if (v.v2 && a.l2_window_bytes > 0) {
+        // pinned factor block: persisting hits in the set-aside L2, streaming misses
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kWarpsPerCta * 32);
+        cfg.dynamicSmemBytes = v.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(a.l2_window_base);
+        attr[0].val.accessPolicyWindow.num_bytes = (size_t)a.l2_window_bytes;
+        attr[0].val.accessPolicyWindow.hitRatio = a.l2_window_hit_ratio;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKRP_CUDA(cudaLaunchKernelEx(&cfg, v.v2, a, (a.flags & SKRP_FLAG_ADDITIVE) ? 1 : 0));
+    } else if (v.v2) {
         v.v2<<<grid, kWarpsPerCta * 32, v.smem, s>>>(a, (a.flags & SKRP_FLAG_ADDITIVE) ? 1 : 0);
-    else
+    } else {
         v.fn<<<grid, kWarpsPerCta * 32, 0, s>>>(a);
+    }
     SKRP_LAUNCHED("mttkrp_tiles_kernel");
     return SKRP_OK;
 }

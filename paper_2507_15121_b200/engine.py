@@ -74,6 +74,7 @@ class PlatformConfig:
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
+    l2_window_mb: int = 0       # >0: per-group launches with an L2 access-policy window on the pinned block
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -427,7 +428,16 @@ class _ShardExec:
         self.nnz = (int(clip[1] - clip[0]) if clip is not None
                     else int(sum(plan.shards[j].nnz for j in shard_ids)))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
-        if self.blocked and self.det:
+        # L2 window: one launch per group whose pinned block gets an access-policy
+        # window (persisting set-aside L2); pin-one-stream-one layouts only
+        self.window = None
+        if cfg.l2_window_mb > 0 and self.blocked and not self.det and plan.block_shifts is not None:
+            ins = [w for w in range(len(plan.shape)) if w != plan.mode and plan.block_shifts[w] >= 0]
+            if len(ins) == 1:
+                self.window = (ins[0], plan.block_shifts[ins[0]])
+                got = ctypes.c_int64()
+                _lib.call("skrp_set_l2_persisting", cfg.l2_window_mb << 20, ctypes.byref(got))
+        if self.blocked and (self.det or self.window is not None):
             keys = sorted({int(k) for j in shard_ids if plan.shards[j].nnz for k in plan.groups[j][:, 2]})
         else:
             keys = [None]
@@ -436,7 +446,7 @@ class _ShardExec:
             tiles, per_shard = tile_table(plan, shard_ids, self.tile_nnz, group_key=key, clip=clip)
             if len(tiles) == 0:
                 continue
-            seg = {"n": len(tiles) // 2, "tiles": torch.from_numpy(tiles).to(gpu), "levels": []}
+            seg = {"n": len(tiles) // 2, "tiles": torch.from_numpy(tiles).to(gpu), "levels": [], "key": key}
             if self.det:
                 for table, final in carry_levels(per_shard, cfg.carry_chunk):
                     nch = len(final)
@@ -539,6 +549,14 @@ class _ShardExec:
         for seg in self.segments:
             a.tiles = seg["tiles"].data_ptr()
             a.num_tiles = seg["n"]
+            if self.window is not None and seg["key"] is not None:
+                w, shift = self.window
+                rows = 1 << shift
+                lo = seg["key"] * rows
+                n_rows = max(0, min(rows, factors[w].shape[0] - lo))
+                a.l2_window_base = factors[w].data_ptr() + lo * self.rank * 4
+                a.l2_window_bytes = n_rows * self.rank * 4
+                a.l2_window_hit_ratio = 1.0
             _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
             if not self.det:
                 continue
@@ -839,7 +857,7 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
 
 def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
     key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout,
-           clip, cfg.col_passes, cfg.col_planes)
+           clip, cfg.col_passes, cfg.col_planes, cfg.l2_window_mb)
     ex = plan._exec_cache.get(key)
     if ex is None:
         if plan.layout == "panel":

@@ -72,7 +72,8 @@ def main():
             cache_key = key
         pl = sk.PlatformConfig(devices=1, rank=R, accumulation=sp.get("acc", "atomic"), tile_nnz=sp.get("tile", 0),
                                kernel_variant=sp.get("variant", 0), col_passes=sp.get("passes", 1),
-                               col_planes=sp.get("planes", True), panel_lockstep=sp.get("lockstep", True))
+                               col_planes=sp.get("planes", True), panel_lockstep=sp.get("lockstep", True),
+                               l2_window_mb=sp.get("window_mb", 0))
         if plan.layout == "panel":
             ex = _PanelExec(plan, list(range(plan.shard_count)), pl, R, dev)
         else:

@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     const int col = sl * VEC;
     const int mode = a.mode;
     const size_t fld = a.factor_ld > 0 ? (size_t)a.factor_ld : (size_t)RR;
+    // factor row address = lane's column base + idx * row pitch in bytes: one
+    // IMAD.WIDE.U32 (u32 x u32 + u64) per gather instead of a 64-bit multiply,
+    // shift and carry chain (4 instructions) with the size_t pitch
+    const uint32_t fld_bytes = (uint32_t)(fld * sizeof(float));
     const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
     const bool additive = (a.flags & SKRP_FLAG_ADDITIVE) != 0;
     const uint32_t *__restrict__ rowc = a.coords[mode];
@@ -88,6 +92,12 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
         F[j] = a.factors[w];
         C[j] = a.coords[w];
     }
+    const char *Fcol[NIN];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) Fcol[j] = reinterpret_cast<const char *>(F[j] + col);
+    auto frow = [&](int j, uint32_t idx) {
+        return reinterpret_cast<const float *>(Fcol[j] + (uint64_t)idx * fld_bytes);
+    };
     const int64_t per_item = (int64_t)pa.groups * NW + 1;
 
     // the panel starts zeroed; every item zeroes the rows it used on the way out
@@ -182,8 +192,8 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, l_c[u / LPN][j], src);
-                        if constexpr (L1NA) ld_row8_na(gv[u][j], F[j] + (size_t)idx * fld + col, pol_row);
-                        else ld_row<VEC>(gv[u][j], F[j] + (size_t)idx * fld + col, 0);
+                        if constexpr (L1NA) ld_row8_na(gv[u][j], frow(j, idx), pol_row);
+                        else ld_row<VEC>(gv[u][j], frow(j, idx), 0);
                     }
                 }
 #pragma unroll
@@ -374,9 +384,9 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
 #pragma unroll
                         for (int j = 0; j < NIN; ++j) {
                             const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                            if constexpr (L1NA) ld_row8_na(gv[u][j], F[j] + (size_t)idx * fld + col, pol_row);
-                            else if ((SM >> j) & 1) ld_row8_first(gv[u][j], F[j] + (size_t)idx * fld + col);
-                            else ld_row<VEC>(gv[u][j], F[j] + (size_t)idx * fld + col, 0);
+                            if constexpr (L1NA) ld_row8_na(gv[u][j], frow(j, idx), pol_row);
+                            else if ((SM >> j) & 1) ld_row8_first(gv[u][j], frow(j, idx));
+                            else ld_row<VEC>(gv[u][j], frow(j, idx), 0);
                         }
                     }
                     if (cls == 0) {

@@ -72,6 +72,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     // row pitches: column passes read an RR-wide slice of wider factor rows
     // (or a column plane) and write an RR-wide slice of wider output rows
     const size_t fld = a.factor_ld > 0 ? (size_t)a.factor_ld : (size_t)RR;
+    // factor row address = lane's column base + idx * row pitch in bytes: one
+    // IMAD.WIDE.U32 (u32 x u32 + u64) per gather instead of a 64-bit multiply,
+    // shift and carry chain (4 instructions) with the size_t pitch
+    const uint32_t fld_bytes = (uint32_t)(fld * sizeof(float));
     const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
     const uint32_t *__restrict__ rowc = a.coords[mode];
     const uint64_t pol_stream = policy_evict_first();
@@ -91,6 +95,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         F[j] = a.factors[w];
         C[j] = a.coords[w];
     }
+    const char *Fcol[NIN];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) Fcol[j] = reinterpret_cast<const char *>(F[j] + col);
+    auto frow = [&](int j, uint32_t idx) {
+        return reinterpret_cast<const float *>(Fcol[j] + (uint64_t)idx * fld_bytes);
+    };
 
     for (;;) {
         unsigned long long claimed = 0;
@@ -251,20 +261,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                         // PLAIN: 1 = no L2 hint on every input; bits 1/2 (+4) mark
                         // input 0/1 as streamed (evict_first 4-bit variants) so it
                         // does not displace the pinned block of the other input
-                        if constexpr (PLAIN == 1) ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                        if constexpr (PLAIN == 1) ld_row8_plain(g[u][j], frow(j, idx));
                         else if constexpr (PLAIN >= 2) {
                             // bit 4 (16): no L1 allocation for any gather
                             if ((PLAIN >> (j + 1)) & 1) {
                                 if constexpr ((PLAIN & 8) && (PLAIN & 16))
-                                    ld_row8_first_na(g[u][j], F[j] + (size_t)idx * fld + col);
-                                else if constexpr (PLAIN & 8) ld_row8_first(g[u][j], F[j] + (size_t)idx * fld + col);
-                                else ld_row8_plain(g[u][j], F[j] + (size_t)idx * fld + col);
+                                    ld_row8_first_na(g[u][j], frow(j, idx));
+                                else if constexpr (PLAIN & 8) ld_row8_first(g[u][j], frow(j, idx));
+                                else ld_row8_plain(g[u][j], frow(j, idx));
                             } else {
-                                if constexpr (PLAIN & 16) ld_row8_last_na(g[u][j], F[j] + (size_t)idx * fld + col);
-                                else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                                if constexpr (PLAIN & 16) ld_row8_last_na(g[u][j], frow(j, idx));
+                                else ld_row<VEC>(g[u][j], frow(j, idx), pol_row);
                             }
                         }
-                        else ld_row<VEC>(g[u][j], F[j] + (size_t)idx * fld + col, pol_row);
+                        else ld_row<VEC>(g[u][j], frow(j, idx), pol_row);
                     }
                 }
                 if (cls == 0) {

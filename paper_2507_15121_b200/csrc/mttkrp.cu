@@ -345,11 +345,11 @@ static Variant mk()
     return v;
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0, int TRED = 0>
 static Variant mk2()
 {
     Variant v;
-    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL, PF>;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL, PF, TRED>;
     v.smem = v2_smem_bytes<8 * LPN>();
     return v;
 }
@@ -360,8 +360,10 @@ static bool pick_v2(int R, Variant &v)
     switch (R) {
     case 8: v = mk2<NM, 1, 1, 3>(); return true;
     case 16: v = mk2<NM, 2, (NM == 3 ? 2 : 1), 3>(); return true;
-    case 32: v = (NM == 3) ? mk2<NM, 4, 4, 2>() : mk2<NM, 4, 2, 3>(); return true;
-    case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2>(); return true;
+    // transpose-reduce row ends (TRED) where VEC >= slots: 7 shuffles + 7 adds
+    // per row end instead of 24 + 24 (R=32), 1-2 % per mode on cfg2
+    case 32: v = (NM == 3) ? mk2<NM, 4, 4, 2, 0, 1, 0, 1>() : mk2<NM, 4, 2, 3, 0, 1, 0, 1>(); return true;
+    case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2, 0, 1, 0, 1>(); return true;
     case 128: v = mk2<NM, 16, (NM == 3 ? 2 : 1), 2>(); return true;
     default: return false;
     }
@@ -435,6 +437,12 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 19 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 2>();
         if (a.variant == 20 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 4>();
         if (a.variant == 21 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 10>();
+        if (a.variant == 25 && a.rank == 32 && a.nmodes == 3) {  // transpose-reduce row ends
+            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10, 1, 0, 1>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 12, 1, 0, 1>();
+            return mk2<3, 4, 4, 2, 0, 1, 0, 1>();
+        }
         if (a.variant == 24 && a.rank == 32 && a.nmodes == 3) {  // + no L1 allocation for the gathers
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 26>();
@@ -459,8 +467,8 @@ static Variant choose(const skrp_mttkrp_args &a)
         }
         if (a.variant == 0 && a.nmodes == 3 && a.rank == 32) {
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 12>();
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10, 1, 0, 1>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 12, 1, 0, 1>();
         }
         if (a.variant == 0) {
             if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;

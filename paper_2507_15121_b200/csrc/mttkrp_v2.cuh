@@ -49,7 +49,7 @@ __device__ __forceinline__ void out_rmw(float *p, const float (&v)[VEC], uint64_
     }
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0, int TRED = 0>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     mttkrp_v2_kernel(const skrp_mttkrp_args a, int additive)
 {
@@ -125,6 +125,51 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int off = LPN; off < 32; off <<= 1)
 #pragma unroll
                 for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
+        };
+        // TRED: transpose-reduce across the S slots -- each butterfly round
+        // exchanges only the half of the values the partner keeps (S = 8: 7
+        // shuffles + 7 adds instead of 24 + 24); lane ends with NV = VEC / S
+        // column sums, columns tcol + k (k < NV), and writes them itself
+        constexpr int NV = (TRED && VEC >= S) ? VEC / S : 1;
+        int tcol = 0;
+        auto treduce = [&](float (&v)[NV]) {
+            float w[VEC];
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) w[i] = acc[i];
+            int base = 0;
+#pragma unroll
+            for (int off = 16, h = VEC / 2; off >= LPN; off >>= 1, h >>= 1) {
+                const bool hi = (lane & off) != 0;
+#pragma unroll
+                for (int k = 0; k < h; ++k) {
+                    const float send = hi ? w[k] : w[k + h];
+                    const float keep = hi ? w[k + h] : w[k];
+                    w[k] = keep + __shfl_xor_sync(kFull, send, off);
+                }
+                base += hi ? h : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) v[k] = w[k];
+            tcol = col + base;
+        };
+        auto write_tred = [&](uint32_t row, bool is_head, bool is_tail) {
+            float v[NV];
+            treduce(v);
+            const bool shared = (is_head && prev_row == (int64_t)row) || (is_tail && next_row == (int64_t)row);
+            float *dst = a.out + (size_t)row * old + tcol;
+            if (shared && det) {
+                const int64_t entry = 2 * t + (is_head ? 0 : 1);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) a.carry_vals[(size_t)entry * RR + tcol + k] = v[k];
+                if (lane == 0) a.carry_rows[entry] = (int32_t)row;
+            } else {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    if (additive && det) st_f1_pol(dst + k, dst[k] + v[k], pol_out);
+                    else if (shared || additive) red_add_f1_pol(dst + k, v[k], pol_out);
+                    else st_f1_pol(dst + k, v[k], pol_out);
+                }
+            }
         };
         // register-layout row write (after reduce_slots slot 0 holds the row)
         auto write_regs = [&](uint32_t row, bool is_head, bool is_tail) {
@@ -227,8 +272,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             if (!uniform) {
                 const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
                 if (row0 != cur) {  // cur ended with the previous batch
-                    reduce_slots();
-                    write_regs(cur, head, false);
+                    if constexpr (TRED && VEC >= S) {
+                        write_tred(cur, head, false);
+                    } else {
+                        reduce_slots();
+                        write_regs(cur, head, false);
+                    }
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
                     cur = row0;
@@ -242,8 +291,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                     e_b = __ffs(cm) - 1;
                 } else if (nb > 1) {
                     cls = 2;
-                    reduce_slots();
-                    if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+                    if constexpr (TRED && VEC >= S) {
+                        float v[NV];
+                        treduce(v);
+#pragma unroll
+                        for (int k = 0; k < NV; ++k) carry_row[tcol + k] = v[k];
+                    } else {
+                        reduce_slots();
+                        if (slot == 0) store_vec<VEC>(carry_row + col, acc);
+                    }
                 }
             }
 
@@ -323,8 +379,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             if (cls == 0) continue;
             if (cls == 1) {
                 // row cur closed at e_b; the new row continues in registers
-                reduce_slots();
-                write_regs(cur, head, false);
+                if constexpr (TRED && VEC >= S) {
+                    write_tred(cur, head, false);
+                } else {
+                    reduce_slots();
+                    write_regs(cur, head, false);
+                }
                 head = false;
                 cur = __shfl_sync(kFull, r_l, e_b);
 #pragma unroll
@@ -395,8 +455,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
             __syncwarp();
         }
-        reduce_slots();
-        write_regs(cur, head, true);
+        if constexpr (TRED && VEC >= S) {
+            write_tred(cur, head, true);
+        } else {
+            reduce_slots();
+            write_regs(cur, head, true);
+        }
     }
 }
 

@@ -152,7 +152,7 @@ def test_mttkrp_matches_oracle(golden, name, r):
         assert rel_err(got, ref[f"{name}_R{r}_oracle_{d}"]) <= TOL
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 25])
 @pytest.mark.parametrize("acc", ["deterministic-reduce", "atomic"])
 @pytest.mark.parametrize("tile", [1, 7, 32, 33, 1024])
 def test_kernel_variants_and_tiles(golden, variant, acc, tile):

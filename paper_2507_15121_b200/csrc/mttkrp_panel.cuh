@@ -283,6 +283,34 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(kFull, acc[i], off);
             };
+            // transpose-reduce (as in mttkrp_v2): lanes end with their own
+            // column sums and add them to the panel row themselves
+            constexpr int NV = (VEC >= S) ? VEC / S : 1;
+            auto reduce_write = [&](uint32_t row) {
+                if constexpr (VEC >= S) {
+                    float w[VEC];
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) w[i] = acc[i];
+                    int base = 0;
+#pragma unroll
+                    for (int off = 16, h = VEC / 2; off >= LPN; off >>= 1, h >>= 1) {
+                        const bool hi = (lane & off) != 0;
+#pragma unroll
+                        for (int k = 0; k < h; ++k) {
+                            const float send = hi ? w[k] : w[k + h];
+                            const float keep = hi ? w[k + h] : w[k];
+                            w[k] = keep + __shfl_xor_sync(kFull, send, off);
+                        }
+                        base += hi ? h : 0;
+                    }
+                    float *pr = prow(row) + col + base;
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) pr[k] += w[k];
+                } else {
+                    reduce_slots();
+                    if (slot == 0) rmw_add_vec<VEC>(prow(row) + col, acc);
+                }
+            };
             auto write_regs = [&](uint32_t row) {  // slot 0 holds the reduced row
                 if (slot == 0) rmw_add_vec<VEC>(prow(row) + col, acc);
             };
@@ -343,8 +371,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                 if (!uniform) {
                     const uint32_t row0 = __shfl_sync(kFull, r_l, 0);
                     if (row0 != cur) {
-                        reduce_slots();
-                        write_regs(cur);
+                        reduce_write(cur);
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
                         cur = row0;
@@ -466,8 +493,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                 for (int g0 = 0; g0 < nin; g0 += G) group(g0);
                 if (cls == 0) continue;
                 if (cls == 1) {
-                    reduce_slots();
-                    write_regs(cur);
+                    reduce_write(cur);
                     cur = __shfl_sync(kFull, r_l, e_b);
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) acc[i] = accB[i];
@@ -546,8 +572,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                 for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
                 __syncwarp();
             }
-            reduce_slots();
-            write_regs(cur);
+            reduce_write(cur);
             __syncwarp();
         }
         __syncthreads();

@@ -496,15 +496,20 @@ struct PanelVariant {
     size_t stage = 0;
 };
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0, int NOTRED = 0>
 static PanelVariant mkp()
 {
-    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF, SM>, NW, 8 * LPN,
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF, SM, NOTRED>, NW, 8 * LPN,
                         panel_stage_bytes<8 * LPN, NW, ALG>()};
 }
 
 static PanelVariant choose_panel(int nmodes, int rank, int variant = 0, int flags = 0)
 {
+    if (nmodes == 3 && rank == 32 && variant == 9) {  // A/B: full-butterfly row ends
+        const int sm = flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+        if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 0, 0, 0, 1, 1>();
+        if (sm == SKRP_FLAG_STREAM_INPUT1) return mkp<3, 4, 4, 16, 0, 0, 0, 2, 1>();
+    }
     if (nmodes == 3 && rank == 32 && variant == 0) {  // streamed input: evict_first loads
         const int sm = flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
         if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 0, 0, 0, 1>();

@@ -47,7 +47,7 @@ __device__ __forceinline__ void grid_wait(unsigned long long *counter, unsigned 
     }
 }
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0>
+template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0, int NOTRED = 0>
 __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     mttkrp_panel_kernel(const skrp_mttkrp_args a, const skrp_panel_args pa)
 {
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             // column sums and add them to the panel row themselves
             constexpr int NV = (VEC >= S) ? VEC / S : 1;
             auto reduce_write = [&](uint32_t row) {
-                if constexpr (VEC >= S) {
+                if constexpr (VEC >= S && !NOTRED) {
                     float w[VEC];
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) w[i] = acc[i];

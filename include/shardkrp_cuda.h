@@ -75,7 +75,7 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 5: per-launch L2 access-policy window in skrp_mttkrp_args */
+int skrp_abi_version(void);  /* 6: skrp_mttkrp_args with the L2 window fields */
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200
@@ -153,7 +153,7 @@ typedef struct {
                                                 misses stream; 0 bytes = none        */
     int64_t l2_window_bytes;
     float l2_window_hit_ratio;
-    int32_t reserved2;
+    int32_t reserved2;                       /* 0 */
 } skrp_mttkrp_args;
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);

@@ -32,7 +32,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 5  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 6  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):

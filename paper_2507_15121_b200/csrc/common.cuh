@@ -137,6 +137,14 @@ __device__ __forceinline__ void ld_row8_first(float (&v)[8], const float *p)
         : "l"(p));
 }
 
+// factor row with a per-lane L2 policy operand (createpolicy value)
+__device__ __forceinline__ void ld_row8_hint(float (&v)[8], const float *p, uint64_t pol)
+{
+    asm("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p), "l"(pol));
+}
+
 __device__ __forceinline__ void ld_row8_first_na(float (&v)[8], const float *p)
 {
     asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"

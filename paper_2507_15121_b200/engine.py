@@ -527,6 +527,7 @@ class _ShardExec:
         a.persistent_ctas = 0
         a.variant = cfg.kernel_variant
         a.flags = self.flags
+
         if events is not None:
             events[0].record()  # current stream == `stream` (callers launch on it)
         if self.passes > 1:

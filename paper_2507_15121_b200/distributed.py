@@ -445,19 +445,23 @@ class DistributedMttkrp:
             comp.wait_event(ev_in[b])
             if k >= 2:
                 comp.wait_event(ev_out[b])  # step k-2's download of this output set is done
-            self.run(fac_sets[b], chained=chained, outputs=out_sets[b])
+
+            def download(d, o, b=b):
+                # mode d's rows leave as soon as they are final, so only the
+                # last mode's download is left to drain after the step
+                s_out.wait_stream(comp)
+                with torch.cuda.stream(s_out):
+                    for lo, hi in spans[d]:
+                        host_outputs[b][d][lo:hi].copy_(o[lo:hi], non_blocking=True)
+
+            self.run(fac_sets[b], chained=chained, outputs=out_sets[b], after_mode=download)
             ev_comp[b].record(comp)
+            ev_out[b].record(s_out)
             if k + 1 < steps:
                 nb = 1 - b
                 if k >= 1:
                     s_in.wait_event(ev_comp[nb])  # step k-1 finished reading that factor set
                 upload(nb)
-            s_out.wait_event(ev_comp[b])
-            with torch.cuda.stream(s_out):
-                for d, (ho, o) in enumerate(zip(host_outputs[b], out_sets[b])):
-                    for lo, hi in spans[d]:
-                        ho[lo:hi].copy_(o[lo:hi], non_blocking=True)
-                ev_out[b].record(s_out)
         comp.wait_stream(s_out)
         comp.wait_stream(s_in)
         return h2d, d2h

@@ -320,7 +320,8 @@ def run_ours(args, cfg):
                            scheduling=args.scheduling,
                            kernel_variant=args.variant,
                            layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
-                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather)
+                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather,
+                           rle_rows=bool(args.rle_rows))
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
@@ -497,6 +498,7 @@ def run_ours(args, cfg):
                                      if any(runner._fused(i) for i in range(len(modes))) else
                                      "NCCL broadcasts of owned row ranges"),
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
+                       "row_ids": "run-length" if pl.rle_rows else "u32 per nonzero",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -766,6 +768,8 @@ def main():
                     help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
+    ap.add_argument("--rle-rows", type=int, default=0, choices=(0, 1),
+                    help="tile kernel reads run-length output-row ids instead of one u32 per nonzero")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     args = ap.parse_args()

@@ -75,7 +75,7 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 6: skrp_mttkrp_args with the L2 window fields */
+int skrp_abi_version(void);  /* 7: skrp_mttkrp_args with the run-length row ids */
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200
@@ -154,7 +154,25 @@ typedef struct {
     int64_t l2_window_bytes;
     float l2_window_hit_ratio;
     int32_t reserved2;                       /* 0 */
+    /* optional run-length output-row ids (tile kernel, R = 32, N = 3; NULL =
+       read coords[mode]): bit k of rle_chg[w] marks nonzero 32w+k as the first
+       of its row (floor(nnz/32)+2 words, tail zero), rle_pre[w] = set bits in
+       words < w, rle_runs[r] = row id of run r.  Built by skrp_rle_mark /
+       skrp_rle_runs; coords[mode] must still hold the same rows. */
+    const uint32_t *rle_chg;
+    const uint32_t *rle_pre;
+    const uint32_t *rle_runs;
 } skrp_mttkrp_args;
+
+/* Run-length output-row ids for skrp_mttkrp_args.rle_* (built once per plan
+ * layout; the reference reads the row coordinate per nonzero, kernels.py:
+ * 54-71).  W = n/32 + 2 words.  skrp_rle_mark: change bits chg[W] (tail words
+ * zero) and per-word run counts counts[W]; the caller exclusive-scans counts
+ * (skrp_exclusive_scan_i64) into prefix[W+1] (prefix[W] = number of runs) and
+ * skrp_rle_runs writes pre[W] (u32 prefix) and runs[prefix[W]].  n < 2^32. */
+int skrp_rle_mark(const uint32_t *rows, int64_t n, uint32_t *chg, int64_t *counts, skrp_stream_t stream);
+int skrp_rle_runs(const uint32_t *rows, int64_t n, const uint32_t *chg, const int64_t *prefix, uint32_t *pre,
+                  uint32_t *runs, skrp_stream_t stream);
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);
 

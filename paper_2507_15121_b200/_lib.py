@@ -32,7 +32,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 6  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 7  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -60,6 +60,9 @@ class MttkrpArgs(ctypes.Structure):
         ("l2_window_bytes", i64),
         ("l2_window_hit_ratio", ctypes.c_float),
         ("reserved2", i32),
+        ("rle_chg", vp),
+        ("rle_pre", vp),
+        ("rle_runs", vp),
     ]
 
 
@@ -110,6 +113,8 @@ SIGNATURES = {
     "skrp_stable_sort_by_key": (i32, [vp, i64, ctypes.c_int, vp, vp, vp, sz, vp]),
     "skrp_gather_u32": (i32, [vp, vp, i64, vp, vp]),
     "skrp_block_keys": (i32, [vp, i32, vp, vp, vp, i64, i32, i64, vp, vp]),
+    "skrp_rle_mark": (i32, [vp, i64, vp, vp, vp]),
+    "skrp_rle_runs": (i32, [vp, i64, vp, vp, vp, vp, vp]),
     "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
     "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, i32, vp]),
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),

@@ -465,6 +465,12 @@ static Variant choose(const skrp_mttkrp_args &a)
             if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
             if (a.nmodes == 4) return mk2<4, 8, 4, 1>();
         }
+        if (a.variant == 0 && a.nmodes == 3 && a.rank == 32 && a.rle_runs) {  // run-length row ids
+            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 42, 1, 0, 1>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 44, 1, 0, 1>();
+            return mk2<3, 4, 4, 2, 32, 1, 0, 1>();
+        }
         if (a.variant == 0 && a.nmodes == 3 && a.rank == 32) {
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10, 1, 0, 1>();

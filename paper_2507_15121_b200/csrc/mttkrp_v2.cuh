@@ -60,6 +60,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     constexpr int STR = RR + 4;     // staging row stride (floats), keeps 16-B alignment
     constexpr int NIN = NM - 1;     // input modes per nonzero
     constexpr int CPL = (RR + 31) / 32;  // columns per lane in the column layout
+    // PLAIN bits 0..4 pick the gather cache policies (below); bit 5 (32) reads
+    // the output-row ids run-length encoded (a.rle_*): change bits + per-word
+    // run prefix + one id per run instead of one u32 per nonzero
+    constexpr int PL = PLAIN & 31;
+    constexpr bool RLE = (PLAIN & 32) != 0;
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
@@ -102,19 +107,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         return reinterpret_cast<const float *>(Fcol[j] + (uint64_t)idx * fld_bytes);
     };
 
+    // row id of nonzero p: the run it lies in is (#change bits at <= p) - 1
+    auto row_at = [&](int64_t p) -> uint32_t {
+        if constexpr (RLE) {
+            const int64_t w = p >> 5;
+            const uint32_t m = __ldg(a.rle_chg + w) & (0xffffffffu >> (31 - (int)(p & 31)));
+            return __ldg(a.rle_runs + __ldg(a.rle_pre + w) + __popc(m) - 1);
+        } else {
+            return rowc[p];
+        }
+    };
+
     for (;;) {
         unsigned long long claimed = 0;
         if (lane == 0) claimed = atomicAdd(a.work_counter, 1ull);
         const int64_t t = (int64_t)__shfl_sync(kFull, claimed, 0);
         if (t >= a.num_tiles) break;
         const int64_t b0 = a.tiles[2 * t], b1 = a.tiles[2 * t + 1];
-        const int64_t prev_row = b0 > 0 ? (int64_t)rowc[b0 - 1] : -1;
-        const int64_t next_row = b1 < a.nnz ? (int64_t)rowc[b1] : -1;
+        const int64_t prev_row = b0 > 0 ? (int64_t)row_at(b0 - 1) : -1;
+        const int64_t next_row = b1 < a.nnz ? (int64_t)row_at(b1) : -1;
         if (det && lane == 0) {
             a.carry_rows[2 * t] = -1;
             a.carry_rows[2 * t + 1] = -1;
         }
-        uint32_t cur = rowc[b0];
+        uint32_t cur = row_at(b0);
         bool head = true;
         float acc[VEC];
 #pragma unroll
@@ -219,7 +235,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
             const bool v = lane < nn;
             const int64_t src = nbase + (v ? lane : nn - 1);
-            r = ld_stream_u32(rowc + src, pol_stream);
+            if constexpr (RLE) {
+                // the batch's 32 change bits straddle two words (uniform loads)
+                const int64_t w = nbase >> 5;
+                const int sh = (int)(nbase & 31);
+                const uint32_t m0 = __ldg(a.rle_chg + w), m1 = __ldg(a.rle_chg + w + 1);
+                const uint32_t win = __funnelshift_r(m0, m1, sh);
+                const uint32_t before = __ldg(a.rle_pre + w) + __popc(m0 & ((1u << sh) - 1u));
+                const int li = v ? lane : nn - 1;
+                r = __ldg(a.rle_runs + before + __popc(win & (0xffffffffu >> (31 - li))) - 1);
+            } else {
+                r = ld_stream_u32(rowc + src, pol_stream);
+            }
             vv_ = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
 #pragma unroll
             for (int j = 0; j < NIN; ++j) c[j] = ld_stream_u32(C[j] + src, pol_stream);
@@ -317,16 +344,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                         // PLAIN: 1 = no L2 hint on every input; bits 1/2 (+4) mark
                         // input 0/1 as streamed (evict_first 4-bit variants) so it
                         // does not displace the pinned block of the other input
-                        if constexpr (PLAIN == 1) ld_row8_plain(g[u][j], frow(j, idx));
-                        else if constexpr (PLAIN >= 2) {
+                        if constexpr (PL == 1) ld_row8_plain(g[u][j], frow(j, idx));
+                        else if constexpr (PL >= 2) {
                             // bit 4 (16): no L1 allocation for any gather
-                            if ((PLAIN >> (j + 1)) & 1) {
-                                if constexpr ((PLAIN & 8) && (PLAIN & 16))
+                            if ((PL >> (j + 1)) & 1) {
+                                if constexpr ((PL & 8) && (PL & 16))
                                     ld_row8_first_na(g[u][j], frow(j, idx));
-                                else if constexpr (PLAIN & 8) ld_row8_first(g[u][j], frow(j, idx));
+                                else if constexpr (PL & 8) ld_row8_first(g[u][j], frow(j, idx));
                                 else ld_row8_plain(g[u][j], frow(j, idx));
                             } else {
-                                if constexpr (PLAIN & 16) ld_row8_last_na(g[u][j], frow(j, idx));
+                                if constexpr (PL & 16) ld_row8_last_na(g[u][j], frow(j, idx));
                                 else ld_row<VEC>(g[u][j], frow(j, idx), pol_row);
                             }
                         }

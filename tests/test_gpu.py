@@ -952,3 +952,81 @@ def test_scaling_floor_per_rank_share():
                                           rank=0, world=1))
     t4 = max(kernel_seconds(DistributedMttkrp(plans, cfg, rank=r, world=4)) for r in range(4))
     assert t1 / t4 > 1.5, (t1, t4)
+
+
+# ------------------------------------------------- run-length output rows
+
+
+def test_rle_arrays_match_rows():
+    """skrp_rle_mark / skrp_rle_runs: change bits, per-word run prefix and run
+    ids reproduce the row array (ragged tail, runs across word boundaries)."""
+    from paper_2507_15121_b200.engine import _plan_rle
+
+    rng = np.random.default_rng(3)
+    for n, shape in ((1, (4, 3, 3)), (31, (7, 5, 5)), (33, (7, 5, 5)), (5000, (40, 30, 30)),
+                     (70_001, (9000, 40, 40))):
+        idx = np.stack([rng.integers(0, s, n) for s in shape], 1).astype(np.uint64)
+        t = sk.SparseTensorCOO(shape, idx, rng.standard_normal(n))
+        p = sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=2))
+        chg, pre, runs = (x.cpu().numpy().view(np.uint32) for x in _plan_rle(p, torch.device("cuda:0")))
+        rows = p.coords[0].cpu().numpy().view(np.uint32)
+        bits = ((chg[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(-1)
+        expect_bits = np.zeros(bits.size, bool)
+        expect_bits[0] = True
+        expect_bits[1:n] = rows[1:] != rows[:-1]
+        assert np.array_equal(bits, expect_bits)
+        assert np.array_equal(runs[: expect_bits.sum()], rows[expect_bits[:n]])
+        pop = np.array([bin(int(w)).count("1") for w in chg])
+        assert np.array_equal(pre, np.concatenate([[0], np.cumsum(pop)[:-1]]).astype(np.uint32))
+        # row of every nonzero from the three arrays (the kernel's row_at)
+        k = np.cumsum(bits)[:n] - 1
+        assert np.array_equal(runs[k], rows)
+
+
+@pytest.mark.parametrize("name", ["u3", "z3"])
+@pytest.mark.parametrize("tile", [16, 100, 4096])
+def test_rle_rows_parity(golden, name, tile):
+    """The tile kernel with run-length row ids (PlatformConfig.rle_rows) gives
+    the oracle's outputs in plan order and the blocked layout, both
+    disciplines; deterministic results are bit-identical to the u32-row path."""
+    t = tensor_from(golden, name)
+    fs = factors_from(golden, name, 32, t.num_modes)
+    ref = golden("mttkrp.npz")
+    for d in range(t.num_modes):
+        for layout in ("flycoo", "blocked"):
+            p = sk.build_mode_plan(t, d, sk.PartitionConfig(devices=2))
+            if layout == "blocked":
+                p.to_blocked([(-1 if w == d else 1) for w in range(t.num_modes)])
+            for acc in ("atomic", "deterministic-reduce"):
+                outs = []
+                for rle in (False, True):
+                    cfg = sk.PlatformConfig(devices=2, rank=32, accumulation=acc, tile_nnz=tile, layout=layout,
+                                            rle_rows=rle)
+                    out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+                    assert rel_err(out, ref[f"{name}_R32_oracle_{d}"]) <= TOL, (layout, acc, rle)
+                    outs.append(out)
+                if acc == "deterministic-reduce":
+                    assert np.array_equal(outs[0], outs[1])
+
+
+def test_rle_rows_streamed_policy_parity():
+    """Run-length row ids with the pin-one-stream-one stream flags (the cfg2
+    default kernels, variants 42/44) on every mode."""
+    from paper_2507_15121_b200.engine import _stream_flags, streamed_blocking
+
+    shape = (2000, 300_000, 280_000)
+    t = sk.synth_tensor_device(shape, 1_500_000, seed=12)
+    fs = sk.random_factors(shape, 32, seed=5)
+    facs = [f.data for f in fs]
+    seen = set()
+    for d in range(3):
+        p = sk.build_mode_plan(t, d, sk.PartitionConfig())
+        sh = streamed_blocking(p, 32)
+        if sh is None:
+            sh = [-1 if w == d else (17 if w == max(w_ for w_ in range(3) if w_ != d) else -1) for w in range(3)]
+        p.to_blocked(sh)
+        seen.add(_stream_flags(p, 32))
+        cfg = sk.PlatformConfig(rank=32, accumulation="atomic", rle_rows=True)
+        out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
+        assert rel_err(out, oracle.mttkrp_seq_c(t.indices, t.values, facs, d)) <= TOL, d
+    assert seen & {_lib.FLAG_STREAM_INPUT0, _lib.FLAG_STREAM_INPUT1}

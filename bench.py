@@ -754,7 +754,7 @@ def main():
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")
     ap.add_argument("--variant", type=int, default=0)
-    ap.add_argument("--parity-rows", type=int, default=512)
+    ap.add_argument("--parity-rows", type=int, default=4096, help="sampled output rows per mode (SURVEY.md §8(c): >= 4096)")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")

@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     constexpr int G = S * U;        // nonzeros per group
     constexpr int RR = VEC * LPN;   // rank handled by this instantiation
     constexpr int STR = RR + 4;     // staging row stride (floats), keeps 16-B alignment
+    // +4 floats for the rows of odd slots (uses the row's 4-float slack)
+    auto srow_skew = [](int e) { return (LPN == 4 && ((e / U) & 1)) ? 4 : 0; };
     constexpr int NIN = NM - 1;     // input modes per nonzero
     constexpr int CPL = (RR + 31) / 32;  // columns per lane in the column layout
     // PLAIN bits 0..4 pick the gather cache policies (below); bit 5 (32) reads
@@ -385,7 +387,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                         }
                     }
                 } else {
-                    // stage each nonzero's contribution row (plain stores)
+                    // stage each nonzero's contribution row (plain stores);
+                    // staged row e starts at e*STR + srow_skew(e): the 2 slots of
+                    // a quarter-warp land in disjoint bank sets (no 2-way
+                    // conflict on the 128-bit stores)
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int e = g0 + slot * U + u;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                             for (int j = 0; j < NIN; ++j) p[i] *= g[u][j][i];
                         }
-                        store_vec<VEC>(stage + e * STR + col, p);
+                        store_vec<VEC>(stage + e * STR + srow_skew(e) + col, p);
                     }
                 }
             };
@@ -439,7 +444,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                 for (int q = 0; q < CPL; ++q) {
                     const int c = lane + 32 * q;
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) sv[q][e] = (c < RR && e < nin) ? stage[e * STR + c] : 0.f;
+                    for (int e = 0; e < 32; ++e)
+                        sv[q][e] = (c < RR && e < nin) ? stage[e * STR + srow_skew(e) + c] : 0.f;
                 }
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) {
                         const int c = lane + 32 * q;
-                        if (c < RR) run[q] += stage[e * STR + c];
+                        if (c < RR) run[q] += stage[e * STR + srow_skew(e) + c];
                     }
                 }
             }

@@ -195,6 +195,20 @@ __device__ __forceinline__ float4 ld_f4_pol(const float *p, uint64_t pol)
     return v;
 }
 
+// a[k] = fma(p[k], g[k], a[k]) where `first`, else b[k] = fma(p[k], g[k], b[k]),
+// k < 4, as predicated FFMAs (one predicate per call): the C form compiles to
+// an FFMA into a temporary + FSEL per element
+__device__ __forceinline__ void fma4_split(bool first, const float *p, const float *g, float *a, float *b)
+{
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %8, 0;\n\t"
+        "@q fma.rn.f32 %0, %9, %13, %0;\n\t@!q fma.rn.f32 %4, %9, %13, %4;\n\t"
+        "@q fma.rn.f32 %1, %10, %14, %1;\n\t@!q fma.rn.f32 %5, %10, %14, %5;\n\t"
+        "@q fma.rn.f32 %2, %11, %15, %2;\n\t@!q fma.rn.f32 %6, %11, %15, %6;\n\t"
+        "@q fma.rn.f32 %3, %12, %16, %3;\n\t@!q fma.rn.f32 %7, %12, %16, %7;\n\t}"
+        : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(b[0]), "+f"(b[1]), "+f"(b[2]), "+f"(b[3])
+        : "r"((int)first), "f"(p[0]), "f"(p[1]), "f"(p[2]), "f"(p[3]), "f"(g[0]), "f"(g[1]), "f"(g[2]), "f"(g[3]));
+}
+
 __device__ __forceinline__ void red_add_f1_pol(float *p, float x, uint64_t pol)
 {
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(x), "l"(pol) : "memory");

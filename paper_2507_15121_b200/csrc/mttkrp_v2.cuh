@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     // run prefix + one id per run instead of one u32 per nonzero
     constexpr int PL = PLAIN & 31;
     constexpr bool RLE = (PLAIN & 32) != 0;
+    // bit 6 (64): class-1 batches accumulate with predicated FFMAs
+    constexpr bool SPLITFMA = (PLAIN & 64) != 0;
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
@@ -377,13 +379,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const bool inA = g0 + slot * U + u < e_b;
+                        float p[VEC];
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) {
-                            float p = vv[u];
+                            p[i] = vv[u];
 #pragma unroll
-                            for (int j = 0; j < NIN - 1; ++j) p *= g[u][j][i];
-                            if (inA) acc[i] = fmaf(p, g[u][NIN - 1][i], acc[i]);
-                            else accB[i] = fmaf(p, g[u][NIN - 1][i], accB[i]);
+                            for (int j = 0; j < NIN - 1; ++j) p[i] *= g[u][j][i];
+                        }
+                        if constexpr (SPLITFMA && VEC % 4 == 0) {
+                            // predicated FFMAs (the select form costs an FSEL per float)
+#pragma unroll
+                            for (int i = 0; i < VEC; i += 4) fma4_split(inA, p + i, g[u][NIN - 1] + i, acc + i, accB + i);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                if (inA) acc[i] = fmaf(p[i], g[u][NIN - 1][i], acc[i]);
+                                else accB[i] = fmaf(p[i], g[u][NIN - 1][i], accB[i]);
+                            }
                         }
                     }
                 } else {

@@ -152,7 +152,7 @@ def test_mttkrp_matches_oracle(golden, name, r):
         assert rel_err(got, ref[f"{name}_R{r}_oracle_{d}"]) <= TOL
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 25])
+@pytest.mark.parametrize("variant", [0, 1, 2, 25, 26])
 @pytest.mark.parametrize("acc", ["deterministic-reduce", "atomic"])
 @pytest.mark.parametrize("tile", [1, 7, 32, 33, 1024])
 def test_kernel_variants_and_tiles(golden, variant, acc, tile):
@@ -896,8 +896,8 @@ def test_plan_cache_reference_files(golden, tmp_path):
         sk.load_plan(bad)
 
 
-@pytest.mark.parametrize("layout", ["blocked", "panel"])
-def test_streamed_input_policy_parity(layout):
+@pytest.mark.parametrize("layout,variant", [("blocked", 0), ("blocked", 26), ("panel", 0)])
+def test_streamed_input_policy_parity(layout, variant):
     """Pin-one-stream-one layouts with factors > 32 MB: the streamed input is
     flagged (SKRP_FLAG_STREAM_INPUTj -> evict_first loads) in the tile and
     panel kernels; every mode matches the oracle."""
@@ -919,7 +919,7 @@ def test_streamed_input_policy_parity(layout):
         else:
             p.to_blocked(sh)
         flags = _stream_flags(p, 32)
-        cfg = sk.PlatformConfig(rank=32, accumulation="atomic")
+        cfg = sk.PlatformConfig(rank=32, accumulation="atomic", kernel_variant=variant)
         out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
         expect = oracle.mttkrp_seq_c(idx, vals, facs, d)
         assert rel_err(out, expect) <= TOL, (layout, d, flags)

@@ -430,14 +430,16 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
                             const bool inA = g0 + (ALG == 2 ? u * S + slot : slot * U + u) < e_b;
+                            float p[VEC];
 #pragma unroll
                             for (int i = 0; i < VEC; ++i) {
-                                float p = vv[u];
+                                p[i] = vv[u];
 #pragma unroll
-                                for (int j = 0; j < NIN - 1; ++j) p *= gv[u][j][i];
-                                if (inA) acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
-                                else accB[i] = fmaf(p, gv[u][NIN - 1][i], accB[i]);
+                                for (int j = 0; j < NIN - 1; ++j) p[i] *= gv[u][j][i];
                             }
+                            // predicated FFMAs, no FSEL per float (as in mttkrp_v2)
+#pragma unroll
+                            for (int i = 0; i < VEC; i += 4) fma4_split(inA, p + i, gv[u][NIN - 1] + i, acc + i, accB + i);
                         }
                     } else if constexpr (ALG == 2) {
                         // one step (S consecutive nonzeros) at a time: stage,

@@ -321,7 +321,7 @@ def run_ours(args, cfg):
                            kernel_variant=args.variant,
                            layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
                            max_blocks=args.max_blocks, fused_allgather=args.fused_allgather,
-                           rle_rows=bool(args.rle_rows))
+                           rle_rows=bool(args.rle_rows), panel_group_sync=bool(args.panel_group_sync))
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
@@ -768,6 +768,8 @@ def main():
                     help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
+    ap.add_argument("--panel-group-sync", type=int, default=0, choices=(0, 1),
+                    help="panel kernel: CTA barrier before every block group")
     ap.add_argument("--rle-rows", type=int, default=0, choices=(0, 1),
                     help="tile kernel reads run-length output-row ids instead of one u32 per nonzero")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),

@@ -208,6 +208,9 @@ typedef struct {
  * and the group's factor blocks stay L2-resident.  Without it CTAs claim items
  * dynamically (better for skewed item sizes). */
 #define SKRP_PANEL_LOCKSTEP 1
+/* ... and the warps of a CTA start every block group together (a CTA barrier
+ * per group), so a CTA never gathers from two groups' blocks at once. */
+#define SKRP_PANEL_GROUP_SYNC 2
 
 int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *panels, skrp_stream_t stream);
 /* warps per CTA and the largest slab the panel kernel supports for (nmodes,

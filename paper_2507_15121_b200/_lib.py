@@ -24,6 +24,7 @@ FLAG_ADDITIVE = 1
 FLAG_STREAM_INPUT0 = 2
 FLAG_STREAM_INPUT1 = 4
 PANEL_LOCKSTEP = 1
+PANEL_GROUP_SYNC = 2
 
 vp = ctypes.c_void_p
 i64 = ctypes.c_int64

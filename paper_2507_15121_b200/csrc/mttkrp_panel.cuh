@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
         reinterpret_cast<float4 *>(panel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     const bool lockstep = (pa.flags & SKRP_PANEL_LOCKSTEP) != 0;
+    const bool group_sync = (pa.flags & SKRP_PANEL_GROUP_SYNC) != 0;
     for (int64_t round = 0;; ++round) {
         __syncthreads();  // previous item's write-back / zeroing done
         int64_t item;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
         };
 
         for (int g = 0; g < pa.groups; ++g) {
+            if (group_sync && g > 0) __syncthreads();  // uniform trip count: every warp arrives
             const int64_t b0 = offs[g * NW + wib], b1 = offs[g * NW + wib + 1];
             if (b0 >= b1) continue;
             if constexpr (ALG == 1) {

@@ -72,6 +72,7 @@ class PlatformConfig:
     slab_rows: int = 0          # panel layout: output rows per slab (0 = auto, see panel_smem_kb)
     panel_smem_kb: int = 64     # panel layout: shared memory for the output panel (auto slab size)
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
+    panel_group_sync: bool = False  # panel layout: a CTA barrier before every block group
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
     l2_window_mb: int = 0       # >0: per-group launches with an L2 access-policy window on the pinned block
@@ -763,7 +764,7 @@ class _PanelExec:
         pa.groups = self.groups
         pa.slab_rows = self.slab_rows
         pa.warps = self.warps
-        pa.flags = _lib.PANEL_LOCKSTEP if self.lockstep else 0
+        pa.flags = (_lib.PANEL_LOCKSTEP if self.lockstep else 0) | (_lib.PANEL_GROUP_SYNC if cfg.panel_group_sync else 0)
         if peers is not None and peers[1]:
             pa.peer_out = peers[0].data_ptr()
             pa.num_peers = peers[1]

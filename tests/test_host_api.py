@@ -420,3 +420,21 @@ def test_spec_acceptance_imbalance():
     assert imbalance(uni, shape, "equal-index") < 5.0
     z = np.stack([np.minimum(rng.zipf(1.2, 200_000) - 1, s - 1) for s in shape], 1)
     assert imbalance(z, shape, "equal-index") > imbalance(z, shape, "nnz-balanced")
+
+
+def test_device_entry_points_validate_before_launch():
+    """Argument checks of device entry points run on the host before any CUDA
+    call: bad sizes map to ValueError with the entry point named (no GPU)."""
+    with pytest.raises(ValueError, match="skrp_rle_mark"):
+        _lib.call("skrp_rle_mark", None, 1 << 32, None, None, None)
+    with pytest.raises(ValueError, match="skrp_rle_runs"):
+        _lib.call("skrp_rle_runs", None, -1, None, None, None, None, None)
+    with pytest.raises(ValueError, match="multiple of 16"):
+        _lib.call("skrp_crc32_chunks", None, 100, 10, None, None)
+    with pytest.raises(ValueError, match="skrp_plan_unpack_indices"):
+        _lib.call("skrp_plan_unpack_indices", None, 10, 0, None, None, None)
+    with pytest.raises(ValueError, match="skrp_f64_to_f32"):
+        _lib.call("skrp_f64_to_f32", None, -5, None, None)
+    # zero-length calls are valid no-ops
+    _lib.call("skrp_crc32_chunks", None, 0, 16, None, None)
+    _lib.call("skrp_f64_to_f32", None, 0, None, None)

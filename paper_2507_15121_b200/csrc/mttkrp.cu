@@ -437,6 +437,14 @@ static Variant choose(const skrp_mttkrp_args &a)
         if (a.variant == 19 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 2>();
         if (a.variant == 20 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 4>();
         if (a.variant == 21 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 10>();
+        if ((a.variant == 27 || a.variant == 28) && a.rank == 32 && a.nmodes == 3) {
+            // A/B: streamed input evict_normal for a hashed 1/2 (27) or 1/4 (28) of its lines
+            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
+            if (a.variant == 27 && sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 202, 1, 0, 1>();
+            if (a.variant == 27 && sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 204, 1, 0, 1>();
+            if (a.variant == 28 && sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 330, 1, 0, 1>();
+            if (a.variant == 28 && sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 332, 1, 0, 1>();
+        }
         if (a.variant == 26 && a.rank == 32 && a.nmodes == 3) {  // + predicated class-1 FFMAs
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 74, 1, 0, 1>();

@@ -88,6 +88,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
     const uint32_t *__restrict__ rowc = a.coords[mode];
     const uint64_t pol_stream = policy_evict_first();
+    // PLAIN bits 7/8 (128/256): the streamed input's rows get evict_normal
+    // for a hashed 1/2 (1/4) of its lines, evict_first for the rest
+    uint64_t pol_sfrac = 0;
+    if constexpr ((PLAIN & 384) == 128)
+        asm("createpolicy.fractional.L2::evict_normal.L2::evict_first.b64 %0, 0.5;" : "=l"(pol_sfrac));
+    else if constexpr ((PLAIN & 384) == 256)
+        asm("createpolicy.fractional.L2::evict_normal.L2::evict_first.b64 %0, 0.25;" : "=l"(pol_sfrac));
     const uint64_t pol_row = policy_evict_last();
     // output rows: evict_first (OUTPOL) so the per-group sweep of output lines
     // does not evict the group's factor blocks; else the default policy
@@ -352,7 +359,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                         else if constexpr (PL >= 2) {
                             // bit 4 (16): no L1 allocation for any gather
                             if ((PL >> (j + 1)) & 1) {
-                                if constexpr ((PL & 8) && (PL & 16))
+                                if constexpr (PLAIN & 384) ld_row8_hint(g[u][j], frow(j, idx), pol_sfrac);
+                                else if constexpr ((PL & 8) && (PL & 16))
                                     ld_row8_first_na(g[u][j], frow(j, idx));
                                 else if constexpr (PL & 8) ld_row8_first(g[u][j], frow(j, idx));
                                 else ld_row8_plain(g[u][j], frow(j, idx));

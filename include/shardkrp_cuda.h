@@ -300,6 +300,11 @@ int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int64_t n, voi
 int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_stream_t stream);
 int skrp_apply_rr(const float *m, int64_t rows, int32_t rank, const double *w, float *out,
                   skrp_stream_t stream);
+/* cpd.py:56-67 in one pass (R = 16/32/64, 16-byte aligned rows): out = m @ w in
+ * fp32, sumsq[R] = fp64 column sums of squares of out (-> lambdas), *nonfinite
+ * = 1 if any element of m is not finite (the MTTKRP output check). */
+int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double *w, float *out, double *sumsq,
+                        int32_t *nonfinite, skrp_stream_t stream);
 int skrp_col_sumsq(const float *x, int64_t rows, int32_t rank, double *out,
                    skrp_stream_t stream);
 int skrp_scale_cols(float *x, int64_t rows, int32_t rank, const double *scale,

@@ -126,6 +126,7 @@ SIGNATURES = {
     "skrp_dedup_mark": (i32, [vp, i32, i64, vp, i64, vp, vp]),
     "skrp_gram": (i32, [vp, i64, i32, vp, vp]),
     "skrp_apply_rr": (i32, [vp, i64, i32, vp, vp, vp]),
+    "skrp_apply_rr_sumsq": (i32, [vp, i64, i32, vp, vp, vp, vp, vp]),
     "skrp_col_sumsq": (i32, [vp, i64, i32, vp, vp]),
     "skrp_scale_cols": (i32, [vp, i64, i32, vp, vp]),
     "skrp_model_inner": (i32, [vp, vp, i64, i32, vp, vp, i32, vp, vp]),

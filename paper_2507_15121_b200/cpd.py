@@ -123,15 +123,31 @@ def _als_update_device(m, grams):
     import torch
 
     rows, rank = m.shape
-    if not np.isfinite(_col_sumsq(m)).all():
-        raise FloatingPointError("non-finite MTTKRP output")
-    v = _hadamard(grams, rank)
-    if not np.isfinite(v).all():
-        raise FloatingPointError("non-finite Gram product")
-    w = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
-    solved = mm_fp32(m, w)  # plain GEMM (rows x R) @ (R x R): cuBLAS fp32
     stream = torch.cuda.current_stream(m.device).cuda_stream
-    lambdas = np.sqrt(_col_sumsq(solved))
+    v = _hadamard(grams, rank)
+    fused = rank in (16, 32, 64) and m.is_contiguous() and m.data_ptr() % 16 == 0
+    if not fused or not np.isfinite(v).all():
+        # reference order (cpd.py): the MTTKRP output is checked before V
+        if not np.isfinite(_col_sumsq(m)).all():
+            raise FloatingPointError("non-finite MTTKRP output")
+        if not np.isfinite(v).all():
+            raise FloatingPointError("non-finite Gram product")
+    if fused:
+        # M @ W, the new columns' sums of squares and the non-finite probe of M
+        # in one pass (skrp_apply_rr_sumsq)
+        w64 = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device)
+        solved = torch.empty_like(m)
+        sq = torch.empty(rank, dtype=torch.float64, device=m.device)
+        bad = torch.empty(1, dtype=torch.int32, device=m.device)
+        _lib.call("skrp_apply_rr_sumsq", m.data_ptr(), rows, rank, w64.data_ptr(), solved.data_ptr(),
+                  sq.data_ptr(), bad.data_ptr(), stream)
+        if int(bad.item()):
+            raise FloatingPointError("non-finite MTTKRP output")
+        lambdas = np.sqrt(sq.cpu().numpy())
+    else:
+        w = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
+        solved = mm_fp32(m, w)  # plain GEMM (rows x R) @ (R x R): cuBLAS fp32
+        lambdas = np.sqrt(_col_sumsq(solved))
     if not np.isfinite(lambdas).all():
         raise FloatingPointError("non-finite entries in updated factor matrix")
     scale = torch.from_numpy(1.0 / np.where(lambdas > 0, lambdas, 1.0)).to(m.device)

@@ -76,6 +76,100 @@ __global__ void __launch_bounds__(256) gram_tiled_kernel(const float *__restrict
     }
 }
 
+// Y^T Y, symmetric and register-tiled (R = 16/32/64): the R x R output is cut
+// into 8x8 tiles and only the UT = T(T+1)/2 upper tiles are computed; a
+// 256-thread block runs GR = 256/UT groups of UT threads, group g taking rows
+// g, g+GR, ... of each staged 128-row tile, so every thread does 64 FMAs per
+// row from 4 LDS.128 (the 4x4-tile kernel above does 16 FMAs per 8 LDS and is
+// shared-memory bound: 4.1 ms for 10 M x 64).  A block owns 1024*GR rows, so
+// every thread sums <= 1024 rows in fp32 (the accuracy contract of
+// gram_tiled_kernel); the GR partials are folded in fp64 in shared memory in a
+// fixed order, then one fp64 atomic per upper entry per block (mirrored after).
+constexpr int kSymTileRows = 128;
+constexpr int kSymRowsPerThread = 1024;
+
+template <int R>
+constexpr int sym_groups()
+{
+    return 256 / ((R / 8) * (R / 8 + 1) / 2);
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 2) gram_sym_kernel(const float *__restrict__ y, int64_t rows, double *g)
+{
+    constexpr int T = R / 8, UT = T * (T + 1) / 2, GR = sym_groups<R>();
+    // the staged rows and (after the row loop) the fp64 group fold share memory
+    constexpr size_t kYs = sizeof(float) * kSymTileRows * R, kRed = sizeof(double) * UT * 64;
+    __shared__ __align__(16) unsigned char smem_raw[kYs > kRed ? kYs : kRed];
+    auto ys = reinterpret_cast<float (*)[R]>(smem_raw);
+    auto red = reinterpret_cast<double (*)[64]>(smem_raw);
+    const int tid = threadIdx.x;
+    const int grp = tid / UT, tix = tid % UT;
+    const bool active = grp < GR;
+    int ti = 0, tj = 0;  // upper tile tix -> (ti, tj), ti <= tj
+    {
+        int k = tix;
+        while (k >= T - ti) { k -= T - ti; ++ti; }
+        tj = ti + k;
+    }
+    float acc[64];
+#pragma unroll
+    for (int k = 0; k < 64; ++k) acc[k] = 0.f;
+    const int64_t b0 = (int64_t)blockIdx.x * ((int64_t)kSymRowsPerThread * GR);
+    const int64_t b1 = b0 + (int64_t)kSymRowsPerThread * GR < rows ? b0 + (int64_t)kSymRowsPerThread * GR : rows;
+    for (int64_t r0 = b0; r0 < b1; r0 += kSymTileRows) {
+        const int nr = (int)((b1 - r0) < kSymTileRows ? (b1 - r0) : kSymTileRows);
+        __syncthreads();
+        for (int i = tid; i < kSymTileRows * R / 4; i += 256) {
+            const int rr = i / (R / 4), c4 = i % (R / 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rr < nr) v = *reinterpret_cast<const float4 *>(y + (r0 + rr) * R + 4 * c4);
+            *reinterpret_cast<float4 *>(&ys[rr][4 * c4]) = v;
+        }
+        __syncthreads();
+        if (active) {
+            for (int rr = grp; rr < nr; rr += GR) {
+                const float4 a0 = *reinterpret_cast<const float4 *>(&ys[rr][ti * 8]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(&ys[rr][ti * 8 + 4]);
+                const float4 c0 = *reinterpret_cast<const float4 *>(&ys[rr][tj * 8]);
+                const float4 c1 = *reinterpret_cast<const float4 *>(&ys[rr][tj * 8 + 4]);
+                const float a_[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float b_[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a * 8 + b] = fmaf(a_[a], b_[b], acc[a * 8 + b]);
+            }
+        }
+    }
+    // fold the GR groups of each tile in shared memory (fixed order)
+    __syncthreads();  // last tile consumed before the buffer turns into `red`
+    for (int gi = 0; gi < GR; ++gi) {
+        __syncthreads();
+        if (active && grp == gi) {
+#pragma unroll
+            for (int k = 0; k < 64; ++k) red[tix][k] = (gi == 0 ? 0.0 : red[tix][k]) + (double)acc[k];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < UT * 64; i += 256) {
+        const int t = i / 64, k = i % 64;
+        int a_t = 0, kk = t;
+        while (kk >= T - a_t) { kk -= T - a_t; ++a_t; }
+        const int b_t = a_t + kk;
+        if (a_t < b_t || (k / 8) <= (k % 8)) atomicAdd(&g[(a_t * 8 + k / 8) * R + b_t * 8 + k % 8], red[t][k]);
+    }
+}
+
+__global__ void gram_mirror_kernel(double *g, int R)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < R * R) {
+        const int r = i / R, c = i % R;
+        if (r > c) g[i] = g[c * R + r];
+    }
+}
+
 // generic fallback (any R <= 64): one thread per (p, q) pair, fp64 sums
 __global__ void __launch_bounds__(256) gram_generic_kernel(const float *__restrict__ y, int64_t rows, int R,
                                                            double *g)
@@ -120,6 +214,103 @@ __global__ void __launch_bounds__(256) apply_rr_tiled_kernel(const float *__rest
 #pragma unroll
             for (int c = 0; c < CG; ++c) out[(r0 + r) * R + cg * CG + c] = acc[c];
         }
+    }
+}
+
+// out = m @ w (w: R x R fp64 on input, applied in fp32 like a plain fp32 GEMM)
+// fused with the column sums of squares of `out` in fp64 (-> lambdas) and an
+// elementwise non-finite probe of `m` (cpd.py: the MTTKRP output check): one
+// pass over m instead of GEMM + two column-norm passes.  Row tiles staged
+// row-major with a 1-float pad (the 4 rows a thread reads per k sit in
+// distinct banks); thread (4 rows x 8 columns) does 32 FMAs per k from 4 LDS +
+// 2 LDS.128.
+// R = 64: 8 rows x 8 columns per thread (64 FMAs per 8 LDS + 2 LDS.128 --
+// the 4-row form was shared-memory bound, ncu: L1 92 %), 128 threads, 120-row
+// tiles (64 x 64 W + 120 x 65 rows fit the 48 KB static limit); R = 16 / 32:
+// 4 rows per thread, 256 threads, 128-row tiles.
+template <int R> struct ApplyCfg {
+    static constexpr int RT = R == 64 ? 8 : 4, NT = R == 64 ? 128 : 256, TR = R == 64 ? 120 : 128;
+};
+
+template <int R>
+__global__ void __launch_bounds__(ApplyCfg<R>::NT) apply_rr_sumsq_kernel(const float *__restrict__ m, int64_t rows,
+                                                             const double *__restrict__ w, float *__restrict__ out,
+                                                             double *__restrict__ sumsq, int *__restrict__ nonfinite)
+{
+    constexpr int CGN = R / 8;            // column groups of 8
+    constexpr int RT = ApplyCfg<R>::RT, NT = ApplyCfg<R>::NT, TR = ApplyCfg<R>::TR;
+    constexpr int RGA = TR / RT;          // active row groups of RT rows
+    static_assert(RGA * CGN <= NT && TR % RT == 0, "tile rows");
+    __shared__ __align__(16) float ws[R][R];
+    __shared__ float ms[TR][R + 1];       // row-major tile; reused for the column fold
+    auto csum = reinterpret_cast<double (*)[8 + 1]>(&ms[0][0]);
+    static_assert(sizeof(double) * RGA * 9 <= sizeof(float) * TR * (R + 1), "fold buffer");
+    for (int i = threadIdx.x; i < R * R; i += NT) ws[i / R][i % R] = (float)w[i];
+    const int cg = threadIdx.x % CGN, rg = threadIdx.x / CGN;
+    const bool active = rg < RGA;
+    double cs[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cs[c] = 0.0;
+    bool bad = false;
+    for (int64_t r0 = (int64_t)blockIdx.x * TR; r0 < rows; r0 += (int64_t)gridDim.x * TR) {
+        const int nr = (int)((rows - r0) < TR ? (rows - r0) : TR);
+        __syncthreads();
+        for (int i = threadIdx.x; i < TR * R / 4; i += NT) {
+            const int rr = i / (R / 4), c4 = i % (R / 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rr < nr) v = *reinterpret_cast<const float4 *>(m + (r0 + rr) * R + 4 * c4);
+            bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+            ms[rr][4 * c4] = v.x;
+            ms[rr][4 * c4 + 1] = v.y;
+            ms[rr][4 * c4 + 2] = v.z;
+            ms[rr][4 * c4 + 3] = v.w;
+        }
+        __syncthreads();
+        if (active) {
+            float acc[RT][8];
+#pragma unroll
+            for (int a = 0; a < RT; ++a)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
+#pragma unroll 4
+            for (int k = 0; k < R; ++k) {
+                float a_[RT];
+#pragma unroll
+                for (int a = 0; a < RT; ++a) a_[a] = ms[rg * RT + a][k];
+                const float4 w0 = *reinterpret_cast<const float4 *>(&ws[k][cg * 8]);
+                const float4 w1 = *reinterpret_cast<const float4 *>(&ws[k][cg * 8 + 4]);
+                const float b_[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int a = 0; a < RT; ++a)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(a_[a], b_[c], acc[a][c]);
+            }
+#pragma unroll
+            for (int a = 0; a < RT; ++a) {
+                if (rg * RT + a < nr) {
+                    float *dst = out + (r0 + rg * RT + a) * R + cg * 8;
+                    *reinterpret_cast<float4 *>(dst) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+                    *reinterpret_cast<float4 *>(dst + 4) = make_float4(acc[a][4], acc[a][5], acc[a][6], acc[a][7]);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) cs[c] += (double)acc[a][c] * (double)acc[a][c];
+                }
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);  // also: tile reads done
+    // fold the row groups per column group, then one fp64 atomic per column
+    for (int cgi = 0; cgi < CGN; ++cgi) {
+        if (cg == cgi && active) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) csum[rg][c] = cs[c];
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            double t = 0.0;
+            for (int r = 0; r < RGA; ++r) t += csum[r][threadIdx.x];
+            atomicAdd(&sumsq[cgi * 8 + threadIdx.x], t);
+        }
+        __syncthreads();
     }
 }
 
@@ -185,6 +376,27 @@ __global__ void scale_cols_kernel(float *x, int64_t rows, int R, const double *_
     int64_t n = rows * R;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         x[i] = (float)((double)x[i] * scale[i % R]);
+}
+
+// R % 4 == 0 and 16-B aligned rows: a thread keeps one float4 column group
+// (and its 4 fp64 scales) for the whole grid-stride loop -- no 64-bit modulo per
+// element; same (float)((double)x * scale) rounding as scale_cols_kernel
+__global__ void __launch_bounds__(256) scale_cols_vec_kernel(float4 *x, int64_t rows, int R,
+                                                             const double *__restrict__ scale)
+{
+    const int q = R / 4;                      // float4 groups per row
+    const int rpb = 256 / q;                  // rows per block pass (q divides 256 for R | 1024)
+    const int c4 = threadIdx.x % q, rr = threadIdx.x / q;
+    if (rr >= rpb) return;
+    const double s0 = scale[4 * c4], s1 = scale[4 * c4 + 1], s2 = scale[4 * c4 + 2], s3 = scale[4 * c4 + 3];
+    for (int64_t i = (int64_t)blockIdx.x * rpb + rr; i < rows; i += (int64_t)gridDim.x * rpb) {
+        float4 v = x[i * q + c4];
+        v.x = (float)((double)v.x * s0);
+        v.y = (float)((double)v.y * s1);
+        v.z = (float)((double)v.z * s2);
+        v.w = (float)((double)v.w * s3);
+        x[i * q + c4] = v;
+    }
 }
 
 struct InnerArgs {
@@ -266,12 +478,26 @@ int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_st
     if (rows == 0) return SKRP_OK;
     SKRP_REQUIRE(y, "skrp_gram: null input");
     unsigned grid = grid_cap((rows + kGramChunk - 1) / kGramChunk, 8);
+    // symmetric register-tiled kernel: a block per 1024*GR rows
+    auto sgrid_for = [&](int gr) { return (unsigned)((rows + (int64_t)kSymRowsPerThread * gr - 1) / ((int64_t)kSymRowsPerThread * gr)); };
+    const bool aligned = ((uintptr_t)y & 15) == 0;
     switch (rank) {
-    case 64: gram_tiled_kernel<64><<<grid, 256, 0, s>>>(y, rows, g_out); break;
-    case 32: gram_tiled_kernel<32><<<grid, 256, 0, s>>>(y, rows, g_out); break;
-    case 16: gram_tiled_kernel<16><<<grid, 256, 0, s>>>(y, rows, g_out); break;
+    case 64:
+        if (aligned) gram_sym_kernel<64><<<sgrid_for(sym_groups<64>()), 256, 0, s>>>(y, rows, g_out);
+        else gram_tiled_kernel<64><<<grid, 256, 0, s>>>(y, rows, g_out);
+        break;
+    case 32:
+        if (aligned) gram_sym_kernel<32><<<sgrid_for(sym_groups<32>()), 256, 0, s>>>(y, rows, g_out);
+        else gram_tiled_kernel<32><<<grid, 256, 0, s>>>(y, rows, g_out);
+        break;
+    case 16:
+        if (aligned) gram_sym_kernel<16><<<sgrid_for(sym_groups<16>()), 256, 0, s>>>(y, rows, g_out);
+        else gram_tiled_kernel<16><<<grid, 256, 0, s>>>(y, rows, g_out);
+        break;
     default: gram_generic_kernel<<<grid_cap(rows, 4), 256, 0, s>>>(y, rows, rank, g_out); break;
     }
+    if (aligned && (rank == 64 || rank == 32 || rank == 16))
+        gram_mirror_kernel<<<(rank * rank + 255) / 256, 256, 0, s>>>(g_out, rank);
     SKRP_LAUNCHED("gram_kernel");
     return SKRP_OK;
 }
@@ -292,6 +518,36 @@ int skrp_apply_rr(const float *m, int64_t rows, int32_t rank, const double *w, f
     default: apply_rr_kernel<<<grid_cap((rows + 7) / 8, 8), 256, 0, s>>>(m, rows, rank, w, out); break;
     }
     SKRP_LAUNCHED("apply_rr_kernel");
+    return SKRP_OK;
+}
+
+int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double *w, float *out, double *sumsq,
+                        int32_t *nonfinite, skrp_stream_t stream)
+{
+    SKRP_REQUIRE((rank == 16 || rank == 32 || rank == 64) && rows >= 0,
+                 "skrp_apply_rr_sumsq: rank must be 16, 32 or 64");
+    SKRP_REQUIRE(sumsq && nonfinite, "skrp_apply_rr_sumsq: null output");
+    cudaStream_t s = (cudaStream_t)stream;
+    SKRP_CUDA(cudaMemsetAsync(sumsq, 0, sizeof(double) * rank, s));
+    SKRP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
+    if (rows == 0) return SKRP_OK;
+    SKRP_REQUIRE(m && w && out && m != out, "skrp_apply_rr_sumsq: bad pointers (in-place not allowed)");
+    SKRP_REQUIRE((((uintptr_t)m | (uintptr_t)out) & 15) == 0, "skrp_apply_rr_sumsq: rows must be 16-byte aligned");
+    switch (rank) {
+    case 64:
+        apply_rr_sumsq_kernel<64><<<grid_cap((rows + 119) / 120, 8), ApplyCfg<64>::NT, 0, s>>>(m, rows, w, out,
+                                                                                           sumsq, nonfinite);
+        break;
+    case 32:
+        apply_rr_sumsq_kernel<32><<<grid_cap((rows + 127) / 128, 4), ApplyCfg<32>::NT, 0, s>>>(m, rows, w, out,
+                                                                                           sumsq, nonfinite);
+        break;
+    default:
+        apply_rr_sumsq_kernel<16><<<grid_cap((rows + 127) / 128, 4), ApplyCfg<16>::NT, 0, s>>>(m, rows, w, out,
+                                                                                           sumsq, nonfinite);
+        break;
+    }
+    SKRP_LAUNCHED("apply_rr_sumsq_kernel");
     return SKRP_OK;
 }
 
@@ -338,8 +594,14 @@ int skrp_scale_cols(float *x, int64_t rows, int32_t rank, const double *scale, s
     SKRP_REQUIRE(rank >= 1 && rows >= 0, "skrp_scale_cols: bad arguments");
     if (rows == 0) return SKRP_OK;
     SKRP_REQUIRE(x && scale, "skrp_scale_cols: null pointer");
-    scale_cols_kernel<<<grid_cap((rows * rank + 255) / 256, 8), 256, 0, (cudaStream_t)stream>>>(x, rows, rank,
-                                                                                                 scale);
+    if (rank % 4 == 0 && 256 % (rank / 4) == 0 && ((uintptr_t)x & 15) == 0) {
+        const int rpb = 256 / (rank / 4);
+        scale_cols_vec_kernel<<<grid_cap((rows + rpb - 1) / rpb, 8), 256, 0, (cudaStream_t)stream>>>(
+            reinterpret_cast<float4 *>(x), rows, rank, scale);
+    } else {
+        scale_cols_kernel<<<grid_cap((rows * rank + 255) / 256, 8), 256, 0, (cudaStream_t)stream>>>(x, rows, rank,
+                                                                                                     scale);
+    }
     SKRP_LAUNCHED("scale_cols_kernel");
     return SKRP_OK;
 }

@@ -621,19 +621,41 @@ class DistributedCpAls:
         for _ in range(iterations):
             for d in range(nm):
                 m = self.mt.mode_output(d, facs)
-                if not np.isfinite(self._col_sumsq(m, d)).all():
-                    raise FloatingPointError("non-finite MTTKRP output")
                 v = _hadamard([grams[w] for w in range(nm) if w != d], R)
-                if not np.isfinite(v).all():
-                    raise FloatingPointError("non-finite Gram product")
-                # owned rows times the R x R inverse: a plain GEMM -> cuBLAS (fp32,
-                # no TF32); everything around it is this package's kernels
-                w_t = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
+                owned = [r for r in self._owned(d) if r[1] > r[0]]
+                # the same decision on every rank (collective sequences must
+                # match): no split boundary rows, whose partial sums count once
+                fused = (R in (16, 32, 64) and m.is_contiguous() and m.data_ptr() % 16 == 0 and np.isfinite(v).all()
+                         and not self.mt.boundary[d])
                 new = torch.empty_like(m)
-                for lo, hi in self._owned(d):
-                    if hi > lo:
+                if fused:
+                    # owned rows times the R x R inverse fused with the new
+                    # columns' sums of squares and the non-finite probe of M
+                    # (skrp_apply_rr_sumsq: one pass instead of GEMM + 2 norms)
+                    w64 = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device)
+                    acc = torch.zeros(R + 1, dtype=torch.float64, device=m.device)
+                    sq = torch.empty(R, dtype=torch.float64, device=m.device)
+                    bad = torch.empty(1, dtype=torch.int32, device=m.device)
+                    for lo, hi in owned:
+                        _lib.call("skrp_apply_rr_sumsq", m[lo:hi].data_ptr(), hi - lo, R, w64.data_ptr(),
+                                  new[lo:hi].data_ptr(), sq.data_ptr(), bad.data_ptr(), stream)
+                        acc[:R] += sq
+                        acc[R] += bad[0].double()
+                    acc = self._allreduce(acc).cpu().numpy()
+                    if acc[R] > 0:
+                        raise FloatingPointError("non-finite MTTKRP output")
+                    lambdas = np.sqrt(acc[:R])
+                else:
+                    if not np.isfinite(self._col_sumsq(m, d)).all():
+                        raise FloatingPointError("non-finite MTTKRP output")
+                    if not np.isfinite(v).all():
+                        raise FloatingPointError("non-finite Gram product")
+                    # owned rows times the R x R inverse: a plain GEMM -> cuBLAS
+                    # (fp32, no TF32)
+                    w_t = torch.from_numpy(np.ascontiguousarray(_solve_matrix(v))).to(m.device, dtype=torch.float32)
+                    for lo, hi in owned:
                         mm_fp32(m[lo:hi], w_t, out=new[lo:hi])
-                lambdas = np.sqrt(self._col_sumsq(new, d))
+                    lambdas = np.sqrt(self._col_sumsq(new, d))
                 if not np.isfinite(lambdas).all():
                     raise FloatingPointError("non-finite entries in updated factor matrix")
                 scale = torch.from_numpy(1.0 / np.where(lambdas > 0, lambdas, 1.0)).to(m.device)

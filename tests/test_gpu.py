@@ -697,6 +697,43 @@ def test_dense_cpd_kernels_vs_numpy():
         assert np.isclose(o.item(), float((y.astype(np.float64) ** 2 @ lam).sum()), rtol=1e-9)
         _lib.call("skrp_sumsq", yt.data_ptr(), rows * R, o.data_ptr(), stream())
         assert np.isclose(o.item(), float((y.astype(np.float64) ** 2).sum()), rtol=1e-9)
+        if R in (16, 32, 64):
+            o2 = torch.empty_like(yt)
+            sq = torch.empty(R, dtype=torch.float64, device="cuda")
+            bad = torch.empty(1, dtype=torch.int32, device="cuda")
+            _lib.call("skrp_apply_rr_sumsq", yt.data_ptr(), rows, R, wt.data_ptr(), o2.data_ptr(), sq.data_ptr(),
+                      bad.data_ptr(), stream())
+            ref2 = y.astype(np.float64) @ w
+            assert np.allclose(o2.cpu().numpy(), ref2, rtol=1e-4, atol=1e-4) and int(bad.item()) == 0
+            assert np.allclose(sq.cpu().numpy(), (o2.cpu().numpy().astype(np.float64) ** 2).sum(0), rtol=1e-12)
+            yb = yt.clone()
+            yb[rows // 2, R - 1] = float("inf")
+            _lib.call("skrp_apply_rr_sumsq", yb.data_ptr(), rows, R, wt.data_ptr(), o2.data_ptr(), sq.data_ptr(),
+                      bad.data_ptr(), stream())
+            assert int(bad.item()) == 1
+        sc = rng.random(R) + 0.5
+        xs = yt.clone()
+        _lib.call("skrp_scale_cols", xs.data_ptr(), rows, R, torch.from_numpy(sc).cuda().data_ptr(), stream())
+        assert np.array_equal(xs.cpu().numpy(), (y.astype(np.float64) * sc).astype(np.float32))
+
+
+@pytest.mark.parametrize("rows,R,offset", [(3_000_001, 64, 0), (1_234_567, 32, 0), (333_333, 16, 0),
+                                           (100_003, 64, 1), (7, 64, 0), (1025 * 7, 64, 0)])
+def test_gram_symmetric_kernel(rows, R, offset):
+    """skrp_gram at scale (register-tiled symmetric kernel for aligned inputs,
+    the 4x4-tile kernel for an unaligned base): fp64 Y^T Y within the fp32
+    partial-sum tolerance, exactly symmetric."""
+    rng = np.random.default_rng(rows)
+    y = (rng.random((rows * R + offset)).astype(np.float32) - 0.25)
+    yt = torch.from_numpy(y).cuda()
+    g = torch.empty((R, R), dtype=torch.float64, device="cuda")
+    _lib.call("skrp_gram", yt.data_ptr() + 4 * offset, rows, R, g.data_ptr(), stream())
+    ym = y[offset:].reshape(rows, R).astype(np.float64)
+    ref = ym.T @ ym
+    got = g.cpu().numpy()
+    if offset == 0:  # the symmetric kernel mirrors its upper triangle
+        assert np.array_equal(got, got.T)
+    assert np.allclose(got, ref, rtol=2e-5, atol=1e-6 * np.abs(ref).max())
 
 
 def test_runner_pipelined_host_path(golden):

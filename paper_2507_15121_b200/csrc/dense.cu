@@ -95,7 +95,8 @@ constexpr int sym_groups()
 }
 
 template <int R>
-__global__ void __launch_bounds__(256, 2) gram_sym_kernel(const float *__restrict__ y, int64_t rows, double *g)
+__global__ void __launch_bounds__(256, 2) gram_sym_kernel(const float *__restrict__ y, int64_t rows, double *g,
+                                                          int rows_per_thread)
 {
     constexpr int T = R / 8, UT = T * (T + 1) / 2, GR = sym_groups<R>();
     // the staged rows and (after the row loop) the fp64 group fold share memory
@@ -115,8 +116,9 @@ __global__ void __launch_bounds__(256, 2) gram_sym_kernel(const float *__restric
     float acc[64];
 #pragma unroll
     for (int k = 0; k < 64; ++k) acc[k] = 0.f;
-    const int64_t b0 = (int64_t)blockIdx.x * ((int64_t)kSymRowsPerThread * GR);
-    const int64_t b1 = b0 + (int64_t)kSymRowsPerThread * GR < rows ? b0 + (int64_t)kSymRowsPerThread * GR : rows;
+    const int64_t span = (int64_t)rows_per_thread * GR;
+    const int64_t b0 = (int64_t)blockIdx.x * span;
+    const int64_t b1 = b0 + span < rows ? b0 + span : rows;
     for (int64_t r0 = b0; r0 < b1; r0 += kSymTileRows) {
         const int nr = (int)((b1 - r0) < kSymTileRows ? (b1 - r0) : kSymTileRows);
         __syncthreads();
@@ -479,19 +481,29 @@ int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_st
     SKRP_REQUIRE(y, "skrp_gram: null input");
     unsigned grid = grid_cap((rows + kGramChunk - 1) / kGramChunk, 8);
     // symmetric register-tiled kernel: a block per 1024*GR rows
-    auto sgrid_for = [&](int gr) { return (unsigned)((rows + (int64_t)kSymRowsPerThread * gr - 1) / ((int64_t)kSymRowsPerThread * gr)); };
+    // <= 1024 rows per thread (the fp32 partial-sum bound), fewer when that
+    // would leave SMs idle (small factors: two blocks per SM)
+    int rpt[3];
+    {
+        const int grs[3] = {sym_groups<64>(), sym_groups<32>(), sym_groups<16>()};
+        for (int q = 0; q < 3; ++q) {
+            const int64_t want = (rows + (int64_t)grs[q] * 296 - 1) / ((int64_t)grs[q] * 296);
+            rpt[q] = (int)std::min<int64_t>(kSymRowsPerThread, std::max<int64_t>(32, want));
+        }
+    }
+    auto sgrid_for = [&](int gr, int r) { return (unsigned)((rows + (int64_t)r * gr - 1) / ((int64_t)r * gr)); };
     const bool aligned = ((uintptr_t)y & 15) == 0;
     switch (rank) {
     case 64:
-        if (aligned) gram_sym_kernel<64><<<sgrid_for(sym_groups<64>()), 256, 0, s>>>(y, rows, g_out);
+        if (aligned) gram_sym_kernel<64><<<sgrid_for(sym_groups<64>(), rpt[0]), 256, 0, s>>>(y, rows, g_out, rpt[0]);
         else gram_tiled_kernel<64><<<grid, 256, 0, s>>>(y, rows, g_out);
         break;
     case 32:
-        if (aligned) gram_sym_kernel<32><<<sgrid_for(sym_groups<32>()), 256, 0, s>>>(y, rows, g_out);
+        if (aligned) gram_sym_kernel<32><<<sgrid_for(sym_groups<32>(), rpt[1]), 256, 0, s>>>(y, rows, g_out, rpt[1]);
         else gram_tiled_kernel<32><<<grid, 256, 0, s>>>(y, rows, g_out);
         break;
     case 16:
-        if (aligned) gram_sym_kernel<16><<<sgrid_for(sym_groups<16>()), 256, 0, s>>>(y, rows, g_out);
+        if (aligned) gram_sym_kernel<16><<<sgrid_for(sym_groups<16>(), rpt[2]), 256, 0, s>>>(y, rows, g_out, rpt[2]);
         else gram_tiled_kernel<16><<<grid, 256, 0, s>>>(y, rows, g_out);
         break;
     default: gram_generic_kernel<<<grid_cap(rows, 4), 256, 0, s>>>(y, rows, rank, g_out); break;

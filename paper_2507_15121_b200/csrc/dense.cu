@@ -316,6 +316,116 @@ __global__ void __launch_bounds__(ApplyCfg<R>::NT) apply_rr_sumsq_kernel(const f
     }
 }
 
+// R = 64 on the tensor cores: 3xTF32 warp MMAs (m16n8k8; a*b ~ ahi*bhi +
+// ahi*blo + alo*bhi, fp32-level accuracy) so the pass is memory-bound instead
+// of FMA / shared-memory bound.  Block = 2 warps, 32-row tiles; warp w owns
+// rows 16w..16w+15 x all 64 columns; W split into tf32 hi/lo once per block.
+__device__ __forceinline__ uint32_t tf32_rna(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+constexpr int kMmaRows = 32, kMmaPad = 68;
+
+__global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__restrict__ m, int64_t rows,
+                                                                const double *__restrict__ w,
+                                                                float *__restrict__ out, double *__restrict__ sumsq,
+                                                                int *__restrict__ nonfinite)
+{
+    constexpr int R = 64;
+    __shared__ __align__(16) uint32_t whi[R][kMmaPad], wlo[R][kMmaPad];
+    __shared__ __align__(16) float ms[kMmaRows][kMmaPad];  // M tile, then the output tile
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    for (int i = tid; i < R * R; i += 64) {
+        const float x = (float)w[i];
+        const uint32_t hi = tf32_rna(x);
+        whi[i / R][i % R] = hi;
+        wlo[i / R][i % R] = tf32_rna(x - __uint_as_float(hi));
+    }
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};  // column sums of squares, columns 4*(tid%16)..+3
+    bool bad = false;
+    for (int64_t r0 = (int64_t)blockIdx.x * kMmaRows; r0 < rows; r0 += (int64_t)gridDim.x * kMmaRows) {
+        const int nr = (int)((rows - r0) < kMmaRows ? (rows - r0) : kMmaRows);
+        __syncthreads();
+        for (int i = tid; i < kMmaRows * R / 4; i += 64) {
+            const int rr = i / (R / 4), c4 = i % (R / 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rr < nr) v = *reinterpret_cast<const float4 *>(m + (r0 + rr) * R + 4 * c4);
+            bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+            *reinterpret_cast<float4 *>(&ms[rr][4 * c4]) = v;
+        }
+        __syncthreads();
+        float acc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+        const int rb = warp * 16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int k0 = kk * 8;
+            const float av[4] = {ms[rb + g][k0 + t], ms[rb + g + 8][k0 + t], ms[rb + g][k0 + t + 4],
+                                 ms[rb + g + 8][k0 + t + 4]};
+            uint32_t ahi[4], alo[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ahi[q] = tf32_rna(av[q]);
+                alo[q] = tf32_rna(av[q] - __uint_as_float(ahi[q]));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t bh0 = whi[k0 + t][j * 8 + g], bh1 = whi[k0 + t + 4][j * 8 + g];
+                const uint32_t bl0 = wlo[k0 + t][j * 8 + g], bl1 = wlo[k0 + t + 4][j * 8 + g];
+                mma_tf32(acc[j], alo, bh0, bh1);
+                mma_tf32(acc[j], ahi, bl0, bl1);
+                mma_tf32(acc[j], ahi, bh0, bh1);
+            }
+        }
+        __syncthreads();  // every warp is done reading its M rows
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            ms[rb + g][j * 8 + 2 * t] = acc[j][0];
+            ms[rb + g][j * 8 + 2 * t + 1] = acc[j][1];
+            ms[rb + g + 8][j * 8 + 2 * t] = acc[j][2];
+            ms[rb + g + 8][j * 8 + 2 * t + 1] = acc[j][3];
+        }
+        __syncthreads();
+        for (int i = tid; i < nr * R / 4; i += 64) {  // i % 16 == tid % 16: fixed column group per thread
+            const int rr = i / (R / 4), c4 = i % (R / 4);
+            const float4 v = *reinterpret_cast<const float4 *>(&ms[rr][4 * c4]);
+            *reinterpret_cast<float4 *>(out + (r0 + rr) * R + 4 * c4) = v;
+            cs[0] += (double)v.x * (double)v.x;
+            cs[1] += (double)v.y * (double)v.y;
+            cs[2] += (double)v.z * (double)v.z;
+            cs[3] += (double)v.w * (double)v.w;
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(nonfinite, 1);
+    // 4 threads share each column group (tid % 16): fold through shared memory
+    double *red = reinterpret_cast<double *>(&ms[0][0]);  // 64 x 4 doubles = 2 KB
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[tid * 4 + q] = cs[q];
+    __syncthreads();
+    if (tid < 16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double v = red[tid * 4 + q] + red[(tid + 16) * 4 + q] + red[(tid + 32) * 4 + q] +
+                             red[(tid + 48) * 4 + q];
+            atomicAdd(&sumsq[4 * tid + q], v);
+        }
+    }
+}
+
 // generic fallback: warp per row, lanes over columns, fp64 accumulation
 __global__ void __launch_bounds__(256) apply_rr_kernel(const float *__restrict__ m, int64_t rows, int R,
                                                        const double *__restrict__ w, float *out)
@@ -533,6 +643,16 @@ int skrp_apply_rr(const float *m, int64_t rows, int32_t rank, const double *w, f
     return SKRP_OK;
 }
 
+// A/B switch for the R = 64 apply: SKRP_APPLY_MMA=0 selects the SIMT kernel
+static bool mma_apply()
+{
+    static const bool on = [] {
+        const char *e = getenv("SKRP_APPLY_MMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double *w, float *out, double *sumsq,
                         int32_t *nonfinite, skrp_stream_t stream)
 {
@@ -547,8 +667,12 @@ int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double
     SKRP_REQUIRE((((uintptr_t)m | (uintptr_t)out) & 15) == 0, "skrp_apply_rr_sumsq: rows must be 16-byte aligned");
     switch (rank) {
     case 64:
-        apply_rr_sumsq_kernel<64><<<grid_cap((rows + 119) / 120, 8), ApplyCfg<64>::NT, 0, s>>>(m, rows, w, out,
-                                                                                           sumsq, nonfinite);
+        if (mma_apply())
+            apply_rr_sumsq_mma_kernel<<<grid_cap((rows + kMmaRows - 1) / kMmaRows, 12), 64, 0, s>>>(m, rows, w, out,
+                                                                                                sumsq, nonfinite);
+        else
+            apply_rr_sumsq_kernel<64><<<grid_cap((rows + 119) / 120, 8), ApplyCfg<64>::NT, 0, s>>>(m, rows, w, out,
+                                                                                               sumsq, nonfinite);
         break;
     case 32:
         apply_rr_sumsq_kernel<32><<<grid_cap((rows + 127) / 128, 4), ApplyCfg<32>::NT, 0, s>>>(m, rows, w, out,

@@ -335,18 +335,25 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-constexpr int kMmaRows = 32, kMmaPad = 68;
+constexpr int kMmaPad = 68;
+constexpr int kMmaWarps = 8;                 // 8 warps x 16 rows = 128-row tiles
+constexpr int kMmaRows = 16 * kMmaWarps;
+constexpr int kMmaThreads = 32 * kMmaWarps;
+constexpr size_t kMmaSmem = sizeof(uint32_t) * 2 * 64 * kMmaPad + sizeof(float) * kMmaRows * kMmaPad;  // 69.6 KB
 
-__global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__restrict__ m, int64_t rows,
-                                                                const double *__restrict__ w,
-                                                                float *__restrict__ out, double *__restrict__ sumsq,
-                                                                int *__restrict__ nonfinite)
+__global__ void __launch_bounds__(kMmaThreads) apply_rr_sumsq_mma_kernel(const float *__restrict__ m, int64_t rows,
+                                                                         const double *__restrict__ w,
+                                                                         float *__restrict__ out,
+                                                                         double *__restrict__ sumsq,
+                                                                         int *__restrict__ nonfinite)
 {
     constexpr int R = 64;
-    __shared__ __align__(16) uint32_t whi[R][kMmaPad], wlo[R][kMmaPad];
-    __shared__ __align__(16) float ms[kMmaRows][kMmaPad];  // M tile, then the output tile
+    extern __shared__ __align__(16) unsigned char mma_smem[];
+    auto whi = reinterpret_cast<uint32_t (*)[kMmaPad]>(mma_smem);
+    auto wlo = reinterpret_cast<uint32_t (*)[kMmaPad]>(mma_smem + sizeof(uint32_t) * 64 * kMmaPad);
+    auto ms = reinterpret_cast<float (*)[kMmaPad]>(mma_smem + sizeof(uint32_t) * 2 * 64 * kMmaPad);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-    for (int i = tid; i < R * R; i += 64) {
+    for (int i = tid; i < R * R; i += kMmaThreads) {
         const float x = (float)w[i];
         const uint32_t hi = tf32_rna(x);
         whi[i / R][i % R] = hi;
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__r
     for (int64_t r0 = (int64_t)blockIdx.x * kMmaRows; r0 < rows; r0 += (int64_t)gridDim.x * kMmaRows) {
         const int nr = (int)((rows - r0) < kMmaRows ? (rows - r0) : kMmaRows);
         __syncthreads();
-        for (int i = tid; i < kMmaRows * R / 4; i += 64) {
+        for (int i = tid; i < kMmaRows * R / 4; i += kMmaThreads) {
             const int rr = i / (R / 4), c4 = i % (R / 4);
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (rr < nr) v = *reinterpret_cast<const float4 *>(m + (r0 + rr) * R + 4 * c4);
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__r
                 mma_tf32(acc[j], ahi, bh0, bh1);
             }
         }
-        __syncthreads();  // every warp is done reading its M rows
+        __syncwarp();  // each warp reads and then overwrites only its own 16 rows
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             ms[rb + g][j * 8 + 2 * t] = acc[j][0];
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__r
             ms[rb + g + 8][j * 8 + 2 * t + 1] = acc[j][3];
         }
         __syncthreads();
-        for (int i = tid; i < nr * R / 4; i += 64) {  // i % 16 == tid % 16: fixed column group per thread
+        for (int i = tid; i < nr * R / 4; i += kMmaThreads) {  // i % 16 == tid % 16
             const int rr = i / (R / 4), c4 = i % (R / 4);
             const float4 v = *reinterpret_cast<const float4 *>(&ms[rr][4 * c4]);
             *reinterpret_cast<float4 *>(out + (r0 + rr) * R + 4 * c4) = v;
@@ -411,16 +418,16 @@ __global__ void __launch_bounds__(64) apply_rr_sumsq_mma_kernel(const float *__r
         }
     }
     if (__syncthreads_or(bad) && tid == 0) atomicOr(nonfinite, 1);
-    // 4 threads share each column group (tid % 16): fold through shared memory
-    double *red = reinterpret_cast<double *>(&ms[0][0]);  // 64 x 4 doubles = 2 KB
+    // kMmaThreads / 16 threads share each column group (tid % 16): fold in smem
+    double *red = reinterpret_cast<double *>(mma_smem);
 #pragma unroll
     for (int q = 0; q < 4; ++q) red[tid * 4 + q] = cs[q];
     __syncthreads();
     if (tid < 16) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double v = red[tid * 4 + q] + red[(tid + 16) * 4 + q] + red[(tid + 32) * 4 + q] +
-                             red[(tid + 48) * 4 + q];
+            double v = 0.0;
+            for (int k = tid; k < kMmaThreads; k += 16) v += red[k * 4 + q];
             atomicAdd(&sumsq[4 * tid + q], v);
         }
     }
@@ -667,9 +674,15 @@ int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double
     SKRP_REQUIRE((((uintptr_t)m | (uintptr_t)out) & 15) == 0, "skrp_apply_rr_sumsq: rows must be 16-byte aligned");
     switch (rank) {
     case 64:
-        if (mma_apply())
-            apply_rr_sumsq_mma_kernel<<<grid_cap((rows + kMmaRows - 1) / kMmaRows, 12), 64, 0, s>>>(m, rows, w, out,
-                                                                                                sumsq, nonfinite);
+        if (mma_apply()) {
+            static const bool attr = [] {
+                return cudaFuncSetAttribute(apply_rr_sumsq_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kMmaSmem) == cudaSuccess;
+            }();
+            SKRP_REQUIRE(attr, "skrp_apply_rr_sumsq: cannot opt in to %zu B of shared memory", kMmaSmem);
+            apply_rr_sumsq_mma_kernel<<<grid_cap((rows + kMmaRows - 1) / kMmaRows, 3), kMmaThreads, kMmaSmem, s>>>(
+                m, rows, w, out, sumsq, nonfinite);
+        }
         else
             apply_rr_sumsq_kernel<64><<<grid_cap((rows + 119) / 120, 8), ApplyCfg<64>::NT, 0, s>>>(m, rows, w, out,
                                                                                                sumsq, nonfinite);

@@ -287,6 +287,79 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------- our arm
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) without torchrun's environment: re-run
+    this script under torch.distributed.run with N ranks on this node (one
+    process per GPU) and return its exit code; None when already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.emulate_world:
+        return None
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL prints the communicator size at init (nRanks) so the driver can
+    # check the collective really spanned N GPUs
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env["BENCH_SELF_LAUNCHED"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def init_dist(args, dev=None):
+    """Process group for N > 1 ranks: NCCL (one GPU per rank) unless
+    BENCH_DIST_BACKEND says otherwise (gloo: CPU tests of the launch path).
+    Fails loudly when the world does not match --gpus or the GPUs are short."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
+    if world == 1:
+        return None
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        if torch.cuda.device_count() < local_world:
+            raise SystemExit(f"bench.py: {local_world} NCCL ranks on this node need as many GPUs, "
+                             f"{torch.cuda.device_count()} visible")
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    if dist.get_world_size() != args.gpus:
+        raise SystemExit(f"bench.py: process group has {dist.get_world_size()} ranks, --gpus {args.gpus}")
+    return dist.get_backend()
+
+
+def launch_check(args):
+    """CPU-testable launch path: every rank joins the group and contributes 1
+    to an all-reduce; rank 0 prints the world it saw (no GPU work)."""
+    import torch
+    import torch.distributed as dist
+
+    backend = init_dist(args) or "none"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    seen = world
+    if world > 1:
+        t = torch.ones(1, dtype=torch.int64)
+        dist.all_reduce(t)
+        seen = int(t.item())
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": seen, "world_size": world, "backend": backend,
+                          "self_launched": os.environ.get("BENCH_SELF_LAUNCHED") == "1"}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -298,15 +371,15 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ngpu = torch.cuda.device_count()
+    if ngpu == 0:
+        raise SystemExit("bench.py: no CUDA device visible (the product path has no CPU fallback)")
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "nccl" and local >= ngpu:
+        raise SystemExit(f"bench.py: local rank {local} has no GPU ({ngpu} visible)")
     local_gpu = local % ngpu  # > 1 rank per GPU only for the gloo smoke of the N>1 path
     torch.cuda.set_device(local_gpu)
     dev = torch.device("cuda", local_gpu)
-    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    backend = init_dist(args, dev) or "none"
 
     def barrier():
         if world > 1:
@@ -431,7 +504,7 @@ def run_ours(args, cfg):
             + sum(shape[w] * R * 4 for w in range(len(shape)) if w != plans[i].mode)
             + runner.owned_rows(i) * R * 4 for i in range(len(modes))]
     balance = plan_balance(plans)
-    kernel_name = "mttkrp_panel_kernel" if plans[0].layout == "panel" else "mttkrp_v2_kernel"
+    kernel_name = {"panel": "mttkrp_panel_kernel", "slots": "mttkrp_slots_kernel"}.get(plans[0].layout, "mttkrp_v2_kernel")
     traffic = lookup_traffic(args.config, kernel_name) if world == 1 else None
 
     # ---- end to end through the public runner with pinned host buffers:
@@ -494,9 +567,11 @@ def run_ours(args, cfg):
                        "parallelism": f"output-row shards x{world}", "scheduling": args.scheduling,
                        "rebalanced_modes": rebalanced,
                        "allgather": ("none (1 GPU)" if world == 1 else
-                                     "fused: panel write-back P2P-stores rows into every rank (CUDA IPC)"
+                                     f"fused: panel write-back P2P-stores rows into every rank (CUDA IPC), "
+                                     f"completion barrier over {backend}"
                                      if any(runner._fused(i) for i in range(len(modes))) else
-                                     "NCCL broadcasts of owned row ranges"),
+                                     f"{backend} broadcasts of owned row ranges"),
+                       "dist_backend": backend, "world_size": world,
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "row_ids": "run-length" if pl.rle_rows else "u32 per nonzero",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
@@ -749,7 +824,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
-    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "auto"))
+    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "slots", "auto"))
     ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")
@@ -774,7 +849,14 @@ def main():
                     help="tile kernel reads run-length output-row ids instead of one u32 per nonzero")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="launch path only: join the process group, all-reduce, print the world seen (CPU ok)")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    if args.launch_check:
+        return launch_check(args)
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         print("note: warmup < 3 is below the timing rules; proceeding", file=sys.stderr)
     cfg = CONFIGS[args.config]

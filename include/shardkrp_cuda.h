@@ -75,7 +75,7 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 7: skrp_mttkrp_args with the run-length row ids */
+int skrp_abi_version(void);  /* 8: slot-owned panels (skrp_slot_args) */
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200
@@ -216,6 +216,39 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
 /* warps per CTA and the largest slab the panel kernel supports for (nmodes,
  * rank); 0 on success, SKRP_ERR_INVALID when no panel kernel exists. */
 int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows);
+
+/* Slot-owned output panels (K1c, csrc/mttkrp_slots.cu; N = 3, R = 32; B200
+ * addition with kernels.py:54-71's per-nonzero arithmetic): an ITEM is the
+ * part of one output slab inside one shard; slot s of the item owns rows
+ * [row_lo + s*rows_per_slot, +rows_per_slot) and its nonzeros are the element
+ * range [slot_offsets[item*(slots+1) + s], slot_offsets[item*(slots+1) + s + 1]) of
+ * the plan arrays, ordered (tile, row) where tile = (c_in0 >> tile_shift0,
+ * c_in1 >> tile_shift1) and in0 < in1 are the input modes.  The arrays must be
+ * readable kWin (skrp_slots_shape chunk_slack) elements past their end.  Every
+ * row of every item is written exactly once (plain stores, also to each
+ * peer_out buffer): no output zeroing, bit-identical for any placement. */
+typedef struct {
+    const int64_t *item_rows;     /* 2*num_items: [row_lo, row_hi)                  */
+    const int64_t *slot_offsets;  /* num_items x (slots_per_item + 1) element offsets */
+    int64_t num_items;
+    int32_t slots_per_item;       /* == skrp_slots_shape slots_per_item              */
+    int32_t rows_per_slot;        /* == skrp_slots_shape rows_per_slot               */
+    int32_t tile_shift0;          /* block shift of input 0 (31: unblocked)          */
+    int32_t tile_shift1;          /* block shift of input 1                          */
+    unsigned int *round_counter;  /* one word of scratch (grid barrier; zeroed here) */
+    const uint64_t *peer_out;     /* num_peers output pointers (CUDA IPC) or NULL    */
+    int32_t num_peers;
+    int32_t reserved;
+} skrp_slot_args;
+int skrp_mttkrp_slots(const skrp_mttkrp_args *args, const skrp_slot_args *slots, skrp_stream_t stream);
+/* layout constants of the slot kernel (N = 3, R = 32 only) */
+int skrp_slots_shape(int32_t nmodes, int32_t rank, int32_t *slots_per_item, int32_t *rows_per_slot,
+                     int32_t *chunk_slack);
+/* key[i] = row_prefix[rows[i]] | (in0[i] >> shift0) << tile_bits1 | (in1[i] >> shift1):
+ * sort keys of the slot layout (row_prefix = (item << slot_bits | slot) << tile bits). */
+int skrp_slot_keys(const uint32_t *rows, const uint32_t *in0, const uint32_t *in1, int64_t n,
+                   const uint32_t *row_prefix, int32_t shift0, int32_t shift1, int32_t tile_bits1, uint32_t *keys,
+                   skrp_stream_t stream);
 
 /* ------------------------------------------------ .tns ingestion (§8(f) 4)
  * GPU restatement of parse_tns (reference tensor.py:173-247).  text: the file

@@ -33,7 +33,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 7  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 8  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -82,6 +82,22 @@ class PanelArgs(ctypes.Structure):
     ]
 
 
+class SlotArgs(ctypes.Structure):
+    _fields_ = [
+        ("item_rows", vp),
+        ("slot_offsets", vp),
+        ("num_items", i64),
+        ("slots_per_item", i32),
+        ("rows_per_slot", i32),
+        ("tile_shift0", i32),
+        ("tile_shift1", i32),
+        ("round_counter", vp),
+        ("peer_out", vp),
+        ("num_peers", i32),
+        ("reserved", i32),
+    ]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
@@ -104,6 +120,9 @@ SIGNATURES = {
     "skrp_set_l2_persisting": (i32, [i64, vp]),
     "skrp_mttkrp_panels": (i32, [vp, vp, vp]),
     "skrp_panel_shape": (i32, [i32, i32, vp, vp]),
+    "skrp_mttkrp_slots": (i32, [vp, vp, vp]),
+    "skrp_slots_shape": (i32, [i32, i32, vp, vp, vp]),
+    "skrp_slot_keys": (i32, [vp, vp, vp, i64, vp, i32, i32, i32, vp, vp]),
     "skrp_device_sm_count": (i32, [ctypes.POINTER(i32)]),
     "skrp_histogram": (i32, [vp, i64, i64, vp, vp]),
     "skrp_scan_workspace_bytes": (sz, [i64]),

@@ -675,10 +675,11 @@ int skrp_apply_rr_sumsq(const float *m, int64_t rows, int32_t rank, const double
     switch (rank) {
     case 64:
         if (mma_apply()) {
-            static const bool attr = [] {
-                return cudaFuncSetAttribute(apply_rr_sumsq_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kMmaSmem) == cudaSuccess;
-            }();
+            // the opt-in is a per-device (per-context) attribute: set it on every
+            // launch (cheap) so a second GPU in the same process is covered
+            const bool attr = cudaFuncSetAttribute(apply_rr_sumsq_mma_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)kMmaSmem) == cudaSuccess;
             SKRP_REQUIRE(attr, "skrp_apply_rr_sumsq: cannot opt in to %zu B of shared memory", kMmaSmem);
             apply_rr_sumsq_mma_kernel<<<grid_cap((rows + kMmaRows - 1) / kMmaRows, 3), kMmaThreads, kMmaSmem, s>>>(
                 m, rows, w, out, sumsq, nonfinite);

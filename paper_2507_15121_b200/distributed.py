@@ -245,7 +245,7 @@ class DistributedMttkrp:
         d_ = _dist()
         self._ipc_bases = []
         for d, out in enumerate(self.outputs):
-            if self.plans[d].layout != "panel":
+            if self.plans[d].layout not in ("panel", "slots"):
                 continue
             h = (ctypes.c_uint8 * 64)()
             off = ctypes.c_int64()

@@ -77,6 +77,7 @@ class PlatformConfig:
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
     l2_window_mb: int = 0       # >0: per-group launches with an L2 access-policy window on the pinned block
     rle_rows: bool = False      # tile kernel reads run-length output-row ids (R=32, N=3)
+    slot_block_shift: int = 0   # slot layout: input blocks of 2^shift rows (0 = auto, 32 MB blocks)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -89,8 +90,8 @@ class PlatformConfig:
             raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
-        if self.layout not in ("flycoo", "blocked", "panel", "auto"):
-            raise ValueError("layout must be 'flycoo', 'blocked', 'panel' or 'auto'")
+        if self.layout not in ("flycoo", "blocked", "panel", "slots", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked', 'panel', 'slots' or 'auto'")
         if self.col_passes < 1 or self.col_passes & (self.col_passes - 1):
             raise ValueError("col_passes must be a power of two >= 1")
 
@@ -352,6 +353,11 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
         return plan
+    if cfg.layout == "slots":
+        if len(plan.shape) != 3 or rank != 32:
+            raise ValueError("slot layout needs N = 3 and R = 32")
+        plan.to_slots(slot_blocking(plan, rank, shift=cfg.slot_block_shift))
+        return plan
     if cfg.layout == "panel":
         prm = choose_panels(plan, rank, cfg, shard_ids)
         if prm is None:
@@ -367,6 +373,10 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
         # skewed rows under deterministic-reduce: plan order + carry tree runs at
         # the atomic speed (cfg4s 28.4 vs 29.2 ms/step, cfg5s 56.6 vs 56.7),
         # the blocked carry path pays per-group launches (123 / 191 ms)
+        return plan
+    if cfg.layout == "auto" and not skewed and slots_apply(plan, rank):
+        # both inputs blocked, output rows in shared memory (K1c): cfg2 modes
+        plan.to_slots(slot_blocking(plan, rank, shift=cfg.slot_block_shift))
         return plan
     if cfg.layout == "auto" and not skewed and len(plan.shape) == 3:
         sh = streamed_blocking(plan, rank)
@@ -391,6 +401,16 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
         else:
             plan.to_blocked(shifts)
     return plan
+
+
+def plan_global_nnz(plan) -> int:
+    """Nonzeros of the WHOLE mode plan (all shards, all ranks): the auto tile
+    size must not depend on the placement, or tile cuts -- and with them the
+    deterministic-reduce carry tree -- would change with the device count."""
+    g = getattr(plan, "global_shard_nnz", None)
+    if g is not None:
+        return int(np.sum(g))
+    return int(sum(s_.nnz for s_ in plan.shards))
 
 
 def auto_tile_nnz(nnz: int, gpu=None) -> int:
@@ -429,7 +449,7 @@ class _ShardExec:
         self.flags = (_lib.FLAG_ADDITIVE if self.blocked else 0) | _stream_flags(plan, rank)
         self.nnz = (int(clip[1] - clip[0]) if clip is not None
                     else int(sum(plan.shards[j].nnz for j in shard_ids)))
-        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
+        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(plan_global_nnz(plan), gpu)
         # L2 window: one launch per group whose pinned block gets an access-policy
         # window (persisting set-aside L2); pin-one-stream-one layouts only
         self.window = None
@@ -621,7 +641,7 @@ class _StreamExec:
         self.passes = 1
         self.levels = []
         self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
-        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(self.nnz, gpu)
+        self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(plan_global_nnz(plan), gpu)
         tiles, _ = tile_table(plan, shard_ids, self.tile_nnz)
         s_, e_ = tiles[0::2], tiles[1::2]
         cap = max(int(cfg.stream_chunk_nnz), self.tile_nnz)
@@ -775,6 +795,91 @@ class _PanelExec:
             events[1].record()
 
 
+class _SlotExec:
+    """Item / slot tables of the slot-owned panel kernel (plan.to_slots) for a
+    set of shards: one launch per mode, every owned row written exactly once
+    (no output zeroing), bit-identical for any placement (DESIGN.md §4 K1c)."""
+
+    writes_all_rows = True
+
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+        torch = _torch()
+        sl = plan.slots
+        self.gpu = gpu
+        self.rank = rank
+        self.det = True
+        self.passes = 1
+        self.levels = []
+        self.tile_nnz = 0
+        mine = np.isin(sl["item_shard"], np.asarray(list(shard_ids), dtype=np.int64))
+        idx = np.nonzero(mine)[0]
+        self.num_items = int(len(idx))
+        self.num_tiles = self.num_items
+        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        self.item_rows = torch.from_numpy(np.ascontiguousarray(sl["item_rows"][idx])).to(gpu)
+        ti = torch.from_numpy(idx).to(sl["slot_offsets"].device)
+        self.slot_offsets = sl["slot_offsets"].index_select(0, ti).to(gpu).contiguous()
+        self.nslot, self.rps = sl["nslot"], sl["rps"]
+        self.shifts = sl["shifts"]
+        self.counter = torch.zeros(1, dtype=torch.int32, device=gpu)
+
+    @property
+    def launches(self) -> int:
+        return 1 if self.num_items else 0
+
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None,
+            peers=None):
+        if self.num_items == 0:
+            return
+        a = _lib.MttkrpArgs()
+        a.nmodes = len(coords)
+        a.mode = mode
+        a.rank = self.rank
+        a.accumulation = _lib.ACC_DETERMINISTIC
+        a.nnz = nnz_total
+        for w, c in enumerate(coords):
+            a.coords[w] = c.data_ptr()
+            a.factors[w] = None if w == mode else factors[w].data_ptr()
+        a.values = vals.data_ptr()
+        a.out = out.data_ptr()
+        sa = _lib.SlotArgs()
+        sa.item_rows = self.item_rows.data_ptr()
+        sa.slot_offsets = self.slot_offsets.data_ptr()
+        sa.num_items = self.num_items
+        sa.slots_per_item = self.nslot
+        sa.rows_per_slot = self.rps
+        sa.tile_shift0, sa.tile_shift1 = self.shifts
+        sa.round_counter = self.counter.data_ptr()
+        if peers is not None and peers[1]:
+            sa.peer_out = peers[0].data_ptr()
+            sa.num_peers = peers[1]
+        if events is not None:
+            events[0].record()
+        _lib.check(_lib.lib().skrp_mttkrp_slots(ctypes.byref(a), ctypes.byref(sa), stream), "skrp_mttkrp_slots")
+        if events is not None:
+            events[1].record()
+
+
+def slot_blocking(plan, rank, block_mb=32, shift=0):
+    """Block shifts of the slot layout: every input factor larger than one
+    block is cut into `block_mb` blocks (2^18 rows at R = 32), the others stay
+    whole (a tile = one block of each input, L2-resident while every SM works
+    on it)."""
+    if shift <= 0:
+        rows = max(1, (block_mb << 20) // (rank * 4))
+        shift = max(0, rows.bit_length() - 1)
+    return [shift if (w != plan.mode and plan.shape[w] > (1 << shift)) else -1 for w in range(len(plan.shape))]
+
+
+def slots_apply(plan, rank) -> bool:
+    """The slot kernel applies: N = 3, R = 32, no row heavier than a slot can
+    carry alone, and inputs too large to stay L2-resident unblocked."""
+    if len(plan.shape) != 3 or rank != 32:
+        return False
+    ins = [w for w in range(3) if w != plan.mode]
+    return sum(plan.shape[w] * rank * 4 for w in ins) > (96 << 20)
+
+
 def panel_shape(nmodes: int, rank: int):
     """(warps per CTA, largest slab rows) of the panel kernel, or None."""
     w = ctypes.c_int32()
@@ -902,6 +1007,10 @@ def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
             if clip is not None:
                 raise ValueError("element-split placement needs the plan-order (flycoo) layout")
             ex = _PanelExec(plan, shard_ids, cfg, rank, gpu)
+        elif plan.layout == "slots":
+            if clip is not None:
+                raise ValueError("element-split placement needs the plan-order (flycoo) layout")
+            ex = _SlotExec(plan, shard_ids, cfg, rank, gpu)
         elif plan.layout == "host":
             if clip is not None:
                 raise ValueError("element-split placement is not streamed")

@@ -205,6 +205,27 @@ def test_device_count_invariance_bit_exact(golden):
             assert np.array_equal(a, b)
 
 
+def test_device_count_invariance_auto_tile():
+    """Default (auto) tile size: it is derived from the whole plan, so 1 and 4
+    devices cut identical tiles and the deterministic carry tree is the same
+    (auto_tile_nnz(10M) = 256 but auto_tile_nnz(10M / 4) = 128)."""
+    from paper_2507_15121_b200.engine import auto_tile_nnz
+
+    nnz = 10_000_000
+    assert auto_tile_nnz(nnz) != auto_tile_nnz(nnz // 4)
+    t = sk.synth_tensor_device((3000, 2000, 1000), nnz, seed=5)
+    fs = sk.random_factors(t.shape, 32, seed=1)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4), keep_permutation=False)
+    results = []
+    for m in (1, 4, 2):
+        cfg = sk.PlatformConfig(devices=m, rank=32)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        results.append(outs)
+    for outs in results[1:]:
+        for a, b in zip(results[0], outs):
+            assert np.array_equal(a, b)
+
+
 def test_write_log_exclusivity(golden):
     t = tensor_from(golden, "u3")
     fs = factors_from(golden, "u3", 8, 3)
@@ -1067,3 +1088,51 @@ def test_rle_rows_streamed_policy_parity():
         out, _ = sk.mttkrp_mode(p, sk.make_devices(fs, cfg), cfg, update_factors=False)
         assert rel_err(out, oracle.mttkrp_seq_c(t.indices, t.values, facs, d)) <= TOL, d
     assert seen & {_lib.FLAG_STREAM_INPUT0, _lib.FLAG_STREAM_INPUT1}
+
+
+# ------------------------------------------------ K1c slot-owned panels
+
+@pytest.mark.parametrize("shift", [0, 9, 11])
+def test_slot_layout_matches_oracle_and_is_placement_invariant(shift):
+    """Slot-owned panel kernel (csrc/mttkrp_slots.cu, plan.to_slots): chained
+    all-mode MTTKRP against the fp64 oracle (cli.py:247-261 metric), host
+    views unchanged by the reorder, and bit-identical outputs for 1, 2 and 4
+    devices (each row's sum order depends on its own nonzeros only)."""
+    shape, nnz = (5000, 3000, 2000), 2_000_000
+    t = sk.synth_tensor_device(shape, nnz, seed=21)
+    idx, vals = t.indices, t.values
+    fs = sk.random_factors(shape, 32, seed=4)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=4, isp_capacity=8192))
+    ref_views = [p._indices.copy() for p in plans]
+    results = []
+    for m in (1, 4, 2):
+        cfg = sk.PlatformConfig(devices=m, rank=32, layout="slots", slot_block_shift=shift)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        assert all(p.layout == "slots" for p in plans)
+        results.append(outs)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(idx, vals, facs, d)
+        assert rel_err(results[0][d], expect) <= TOL, (d, rel_err(results[0][d], expect))
+        facs[d] = results[0][d]
+    for outs in results[1:]:
+        for a, b in zip(results[0], outs):
+            assert np.array_equal(a, b)
+    for p, v in zip(plans, ref_views):  # the plan the reference would see is untouched
+        assert np.array_equal(p._indices, v)
+
+
+def test_slot_layout_ragged_shards_and_empty_rows():
+    """Shards of a few rows, items smaller than a slab, rows without nonzeros
+    and a skew that leaves some slots empty: every owned row is written."""
+    shape = (1500, 700, 900)
+    t = sk.synth_tensor_device(shape, 300_000, distribution="zipf", seed=3)
+    fs = sk.random_factors(shape, 32, seed=2)
+    plans = sk.build_all_plans(t, sk.PartitionConfig(devices=3, oversubscription=5, strategy="nnz-balanced"))
+    cfg = sk.PlatformConfig(devices=3, rank=32, layout="slots", slot_block_shift=7)
+    outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(outs[d], expect) <= TOL
+        facs[d] = outs[d]

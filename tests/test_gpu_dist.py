@@ -48,15 +48,21 @@ def _worker(rank, world, port, q):
                                                ((500, 80, 60, 7), 300_000, "zipf", "nnz-balanced")]:
             # the chunk generator reproduces its slice of the global draw stream
             raw = synth_tensor_device(shape, nnz, distribution=dist_law, seed=6, unique=False)
-            ch = synth_tensor_chunk(shape, nnz, rank, world, distribution=dist_law, seed=6)
+            ch = synth_tensor_chunk(shape, nnz, rank, world, distribution=dist_law, seed=6, unique=False)
             lo, hi = nnz * rank // world, nnz * (rank + 1) // world
             rc, rv = raw.device_arrays()
             cc, cv = ch.device_arrays()
             assert all(torch.equal(a[lo:hi], b) for a, b in zip(rc, cc)) and torch.equal(rv[lo:hi], cv)
-            # plans are built from contiguous slices of a de-duplicated tensor
+            # the reference's unique-tuple law across ranks (synth.py:68-84): the
+            # chunks of the globally de-duplicated stream == the 1-GPU generator
             full = synth_tensor_device(shape, nnz, distribution=dist_law, seed=6)
             fc, fv = full.device_arrays()
-            chunk = sk.SparseTensorCOO.from_device(shape, [c[lo:hi].contiguous() for c in fc], fv[lo:hi].contiguous())
+            uq = synth_tensor_chunk(shape, nnz, rank, world, distribution=dist_law, seed=6)
+            uc, uv = uq.device_arrays()
+            assert all(torch.equal(a[lo:hi], b) for a, b in zip(fc, uc)) and torch.equal(fv[lo:hi], uv)
+            if dist_law == "zipf":
+                assert full.stats.duplicates > 0  # the law really rejected draws here
+            chunk = uq
             pcfg = sk.PartitionConfig(devices=world, strategy=strategy, isp_capacity=1000)
             ref_plans = sk.build_all_plans(full, pcfg)
             plans = [build_mode_plan_distributed(chunk, d, pcfg) for d in range(len(shape))]

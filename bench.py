@@ -124,19 +124,80 @@ def plan_balance(plans):
     return out
 
 
-def lookup_traffic(config, kernel):
-    """DRAM read+write bytes per launch of `kernel` on `config` from one ncu
-    --set full capture (profiles/ncu_traffic.json), or None."""
+def kernel_key(name):
+    """Kernel name without return type, namespaces and spaces: the form an
+    ncu 'Kernel Name' and the library's demangled launch log share."""
+    n = name.strip()
+    if n.startswith("void "):
+        n = n[5:]
+    for ns in ("skrp::", "(anonymous namespace)::", "::"):
+        n = n.replace(ns, "")
+    return n.replace(" ", "").replace("const", "")
+
+
+def lookup_traffic(config, mode, kernel):
+    """DRAM read+write bytes per launch of EXACTLY `kernel` (demangled name
+    from the library's launch log) on `config`, mode `mode`, from one ncu
+    --set full capture (profiles/ncu_traffic.json), or (None, reason): an
+    entry for another template instantiation is never reused."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             pj = json.load(fh)
     except Exception:
-        return None
-    for e in pj.get("entries", [pj]):
-        if e.get("config") == config and kernel in e.get("kernel", ""):
-            return e.get("traffic_bytes_per_launch")
-    return None
+        return None, "profiles/ncu_traffic.json unreadable"
+    want = kernel_key(kernel)
+    for e in pj.get("entries", []):
+        if e.get("config") == config and e.get("mode") == mode and kernel_key(e.get("kernel", "")) == want:
+            return e, None
+    return None, f"no ncu capture of {want} on {config} mode {mode}"
+
+
+def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world):
+    """Roofline of the dominant (MTTKRP) kernel per mode.  `frac` uses the
+    bytes the kernel really moves: DRAM read + write per launch from the ncu
+    --set full capture of EXACTLY the launched template instantiation
+    (profiles/ncu_traffic.json, matched through the library's launch log),
+    over the live per-launch time measured here with CUDA events.  The
+    SURVEY.md §8(d) algorithmic figure (every gather charged to HBM; > 1 when
+    L2 serves gathers) is `frac_algorithmic`; the compulsory lower bound
+    (stream once, each factor once, output once) is `frac_compulsory`."""
+    import torch
+
+    from paper_2507_15121_b200 import _lib
+
+    _lib.launch_log(clear=True)
+    runner.run(dev_f)  # one eager pass, untimed: which kernels run per mode
+    torch.cuda.synchronize()
+    log = _lib.launch_log()
+    names = [sorted({n for m, n in log if m == d}) for d in modes]
+    per_mode, traffic, missing = [], [], []
+    for i, d in enumerate(modes):
+        ent, why = (None, "N > 1: ncu captures are single-GPU") if world > 1 else (
+            lookup_traffic(config, d, names[i][0]) if len(names[i]) == 1 else (None, "several kernels per mode"))
+        t = ent["traffic_bytes_per_launch"] if ent else None
+        traffic.append(t)
+        if ent is None:
+            missing.append(why)
+        per_mode.append({"mode": d, "kernel": names[i], "ms": kern[i] * 1e3,
+                         "dram_bytes_ncu": t, "ncu_source": ent.get("source") if ent else None,
+                         "dram_gbs": t / kern[i] / 1e9 if t else None,
+                         "frac_dram": t / kern[i] / 1e9 / peak if t else None,
+                         "frac_algorithmic": alg[i] / kern[i] / 1e9 / peak,
+                         "frac_compulsory": comp[i] / kern[i] / 1e9 / peak})
+    ach_alg = sum(alg) / sum(kern) / 1e9
+    if all(t is not None for t in traffic):
+        achieved, basis = sum(traffic) / sum(kern) / 1e9, "measured DRAM bytes (ncu, same kernel) / live kernel time"
+        tr = sum(traffic) / len(traffic)
+    else:
+        achieved, basis, tr = ach_alg, "algorithmic bytes (SURVEY.md §8(d)): " + "; ".join(missing), None
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": tr, "achieved_basis": basis, "peak_source": peak_src,
+            "kernel": names[0][0] if names and names[0] else None,
+            "kernel_ms_per_mode": [k * 1e3 for k in kern], "algorithmic_bytes_per_mode": alg,
+            "compulsory_bytes_per_mode": comp, "achieved_algorithmic": ach_alg,
+            "frac_algorithmic": ach_alg / peak, "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak,
+            "per_mode": per_mode}
 
 
 def algorithmic_bytes(shape, nnz, rank, mode):
@@ -236,6 +297,66 @@ def cpu_engine_run(shape, nnz, rank, threads, seed=1, steps=1, warmup=0):
 
 # ----------------------------------------------------------- reference arm
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def ref_package_legs(cfg, threads):
+    """The UNMODIFIED reference package (`shardkrp` from baseline/_ref: numba
+    `ec_accumulate` kernels.py:54-71 driven by engine.py:225-400) on a bounded
+    sample of the config, in BASELINE.md §2's two configurations: the CLI
+    defaults (1 simulated device, 1 worker, column_width 32) and the best-tuned
+    one (8 simulated devices, 1 worker each, column_width 8192; more devices
+    only add fp64 ring all-gather copies of the whole factor set per device).
+    One warm-up pass (numba JIT), then the best of two timed passes.  Reports
+    wall time of mttkrp_all_modes and the critical-path compute (max over the
+    simulated devices of their compute seconds, summed over modes)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "shardkrp")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference/pkg)"}
+    if cfg["desc"].split(":")[0] not in ("cfg1", "cfg2") or cfg["dist"] != "uniform":
+        return {"unavailable": "run on the cfg1 / cfg2 headline configs only (bounded CPU time)"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/skrp_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import shardkrp as ref
+
+    shape = cfg["shape"]
+    modes = list(range(len(shape))) if cfg["modes"] is None else cfg["modes"]
+    sample = min(cfg["nnz"], 1_000_000 if len(modes) == 1 else 2_000_000)
+    idx, vals = host_sample(shape, sample, 1)
+    tensor = ref.SparseTensorCOO(shape, idx, vals)
+    legs = []
+    for name, m, cw in (("cli-default", 1, 32), ("best-tuned", min(8, threads), 8192)):
+        pcfg = ref.PartitionConfig(devices=m)
+        plans = [ref.build_mode_plan(tensor, d, pcfg) for d in modes]
+        fs = ref.random_factors(shape, cfg["rank"], seed=0)
+        pl = ref.PlatformConfig(devices=m, workers_per_device=1, rank=cfg["rank"], column_width=cw)
+        best = None
+        for it in range(3):
+            devs = ref.make_devices(fs, pl)
+            t0 = time.perf_counter()
+            _, met = ref.mttkrp_all_modes(plans, devs, pl)
+            wall = time.perf_counter() - t0
+            crit = sum(max(mm.device_compute_seconds) for mm in met.modes)
+            if it >= 1 and (best is None or wall < best[0]):
+                best = (wall, crit)
+        legs.append({"config": name, "devices": m, "workers_per_device": 1, "column_width": cw,
+                     "isp_capacity": pcfg.isp_capacity, "sample_nnz": sample, "modes": modes,
+                     "wall_s": best[0], "nnz_per_s_wall": len(modes) * sample / best[0],
+                     "critical_path_compute_s": best[1], "nnz_per_s_compute": len(modes) * sample / best[1]})
+    return {"kind": "reference", "package": "shardkrp " + getattr(ref, "__version__", "?") + " (baseline/_ref, numba)",
+            "legs": legs}
+
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
@@ -269,17 +390,31 @@ def run_reference(args, cfg):
             t_all.append(dt)
     t = sum(t_all) / len(t_all)
     value = nmodes * sample / t
+    kind, ms = "port", t * 1e3
+    pkg = ref_package_legs(cfg, threads)
+    # the arm reports the FASTER of the reference package (wall time of its own
+    # public mttkrp_all_modes, best-tuned) and the C port: the conservative baseline
+    for leg in pkg.get("legs", []):
+        if leg["nnz_per_s_wall"] > value:
+            value, kind, ms = leg["nnz_per_s_wall"], "reference", leg["wall_s"] * 1e3
+            samp_ref = (f"{leg['sample_nnz']} nnz on the {cfg['desc'].split(':')[0]} shape/law, {nmodes} mode(s); "
+                        f"shardkrp package ({leg['config']}: {leg['devices']} devices, column_width "
+                        f"{leg['column_width']})")
     samp = f"{sample} nnz on the {cfg['desc'].split(':')[0]} shape/law ({'full' if sample == cfg['nnz'] else '1/64'}), {nmodes} mode(s) per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "shape": list(modes_shape), "nnz": cfg["nnz"], "rank": cfg["rank"],
                    "sample_nnz": sample, "partition": "equal-index, devices=cores, oversub 4, ISP 8192"},
-        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
-                         "sample": samp},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads if kind == "port" else None,
+                         "kind": kind, "sample": samp if kind == "port" else samp_ref, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "port": {"value": nmodes * sample / t, "ms_per_step": t * 1e3, "threads": threads, "sample": samp},
+        "reference_package": pkg,
     }
+    if kind == "reference":
+        line["cpu_baseline"]["cores"] = min(8, threads)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -398,6 +533,10 @@ def run_ours(args, cfg):
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
+    verify = rank == 0 and not dist_build and not args.no_parity and not args.stream_modes and not args.emulate_world
+    plan_checks = []
+    if verify:
+        from oracle.scale import sample_parity_source, verify_plan_full
     if world == 1 and cfg.get("dist_build", False):
         raise SystemExit(f"{args.config} does not fit one B200 ({nnz} nnz); run it with torchrun --nproc-per-node >= 2 "
                          f"or use the single-GPU '{args.config}s' variant")
@@ -409,14 +548,26 @@ def run_ours(args, cfg):
 
         tensor = synth_tensor_chunk(shape, nnz, rank, world, distribution=cfg["dist"], seed=0)
         plans = [build_mode_plan_distributed(tensor, d, pcfg, scheduling=args.scheduling) for d in modes]
-    elif cfg["host_gen"]:
-        tensor = sk.synth_tensor(shape, nnz, distribution=cfg["dist"], seed=0)
-        plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
     else:
-        tensor = sk.synth_tensor_device(shape, nnz, distribution=cfg["dist"], seed=0)
-        plans = [sk.build_mode_plan(tensor, d, pcfg, keep_permutation=False) for d in modes]
+        if cfg["host_gen"]:
+            tensor = sk.synth_tensor(shape, nnz, distribution=cfg["dist"], seed=0)
+        else:
+            tensor = sk.synth_tensor_device(shape, nnz, distribution=cfg["dist"], seed=0)
+        plans = []
+        for d in modes:
+            p_ = sk.build_mode_plan(tensor, d, pcfg, keep_permutation=verify)
+            if verify:
+                # full-scale plan properties against the SOURCE arrays (oracle/scale.py),
+                # before any execution-layout reordering; then the permutation goes
+                src_c, src_v = tensor.device_arrays()
+                plan_checks.append(verify_plan_full(src_c, src_v, p_, cfg["strategy"], devices=pcfg.devices,
+                                                    isp_capacity=pcfg.isp_capacity))
+                p_.perm = None
+                torch.cuda.empty_cache()
+            plans.append(p_)
     build_s = [p.build_time for p in plans]
-    tensor.drop_device()
+    if not verify:
+        tensor.drop_device()  # (kept for the source-tensor parity sample otherwise)
     torch.cuda.empty_cache()
     init = sk.random_factors(shape, R, seed=0)
     host_f = [torch.from_numpy(f.data.astype(np.float32)).pin_memory() for f in init]
@@ -438,7 +589,8 @@ def run_ours(args, cfg):
     runner.prepare(R)
     setup_s = time.perf_counter() - t_setup
     if cfg.get("kind") == "cpd":
-        return run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s)
+        return run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s,
+                       tensor=tensor if verify else None, plan_checks=plan_checks)
 
     for _ in range(args.warmup):
         runner.run(dev_f)
@@ -504,8 +656,7 @@ def run_ours(args, cfg):
             + sum(shape[w] * R * 4 for w in range(len(shape)) if w != plans[i].mode)
             + runner.owned_rows(i) * R * 4 for i in range(len(modes))]
     balance = plan_balance(plans)
-    kernel_name = {"panel": "mttkrp_panel_kernel", "slots": "mttkrp_slots_kernel"}.get(plans[0].layout, "mttkrp_v2_kernel")
-    traffic = lookup_traffic(args.config, kernel_name) if world == 1 else None
+    roof = roofline_block(args.config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world)
 
     # ---- end to end through the public runner with pinned host buffers:
     # every step uploads the factors it reads and downloads all outputs;
@@ -537,7 +688,16 @@ def run_ours(args, cfg):
 
     # ---- parity on a seeded sample of output rows (chained replay, fp64)
     parity = None
-    if rank == 0 and not args.no_parity and not streamed:
+    if verify:
+        src_c, src_v = tensor.device_arrays()
+        parity = sample_parity_source(src_c, src_v, shape, [f.data for f in init], runner.outputs, modes,
+                                      rows_per_mode=args.parity_rows)
+        parity["plans"] = plan_checks
+        parity["plans_ok"] = all(c["ok"] for c in plan_checks)
+        tensor.drop_device()
+    elif rank == 0 and not args.no_parity and not streamed:
+        # distributed build: no rank holds the source tensor; rows owned here are
+        # recomputed from this rank's plan arrays
         parity = sample_parity(plans, init, runner.outputs, modes, rows_per_mode=args.parity_rows,
                                owned=[runner.ownership[i][rank] for i in range(len(modes))] if dist_build else None)
 
@@ -549,10 +709,11 @@ def run_ours(args, cfg):
         if cfg["modes"] is not None:
             cpu_v, cpu_t = cpu_mode0(shape, sample, R, threads) if len(modes) == 1 else (None, None)
         else:
-            cpu_v, cpu_t = cpu_engine_run(shape, sample, R, threads)
-        cpu = {"value": cpu_v, "unit": "nnz/s", "cores": threads, "kind": "port",
+            cpu_v, cpu_t = cpu_engine_run(shape, sample, R, threads, steps=2, warmup=1)
+        cpu = {"value": cpu_v, "unit": "nnz/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{sample} nnz, same shape and law, {len(modes)} mode(s), C port of the reference "
-                         f"deterministic-reduce engine (fp64), devices=cores, ISP 8192; {cpu_t:.2f} s/pass"}
+                         f"deterministic-reduce engine (fp64), devices=cores, ISP 8192, 1 warm-up + best of 2; "
+                         f"{cpu_t:.2f} s/pass"}
 
     if rank == 0:
         line = {
@@ -575,15 +736,7 @@ def run_ours(args, cfg):
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
                        "row_ids": "run-length" if pl.rle_rows else "u32 per nonzero",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": kernel_name, "kernel_ms_per_mode": [k * 1e3 for k in kern],
-                         "algorithmic_bytes_per_mode": alg, "compulsory_bytes_per_mode": comp,
-                         "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak,
-                         # measured DRAM bytes of the mode-0 launch (ncu) over its live time: how
-                         # close the kernel runs to the HBM roofline on the bytes it really moves
-                         "dram_gbs_mode0": (traffic / kern[0] / 1e9) if traffic else None,
-                         "frac_dram_mode0": (traffic / kern[0] / 1e9 / peak) if traffic else None},
+            "roofline": roof,
             "balance": balance,
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
@@ -663,7 +816,8 @@ def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
     return 0
 
 
-def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s):
+def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s, tensor=None,
+            plan_checks=()):
     """cfg5: one full CPD-ALS iteration per step (all modes: MTTKRP, solve,
     normalisation, factor all-gather, Grams, fit)."""
     import torch
@@ -705,7 +859,30 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
     kern = [a.elapsed_time(b) / 1e3 for a, b in kev]
     peak, peak_src = load_peaks()
     alg = [runner.algorithmic_bytes(i) for i in range(nm)]
-    achieved = sum(alg) / sum(kern) / 1e9
+    shape, R = cfg["shape"], cfg["rank"]
+    comp = [runner.local_nnz(i) * (4 * nm + 4) + sum(shape[w] * R * 4 for w in range(nm) if w != plans[i].mode)
+            + runner.owned_rows(i) * R * 4 for i in range(nm)]
+    roof = roofline_block(args.config, list(range(nm)), runner, dev_f, kern, alg, comp, peak, peak_src, world)
+    roof["mttkrp_share_of_iteration"] = sum(kern) / step_s
+    parity = None
+    if tensor is not None:
+        # one more iteration with the checker hooked into every mode update:
+        # sampled MTTKRP rows and the ALS update M V^-1 of those rows, in fp64
+        # from the source tensor (oracle/scale.py cpd_mode_check)
+        from oracle.scale import cpd_mode_check
+
+        src_c, src_v = tensor.device_arrays()
+        checks = []
+        als.run(dev_f, iterations=1, observe=lambda d, facs, m, new, lam: checks.append(
+            cpd_mode_check(src_c, src_v, cfg["shape"], d, facs, m, new, lam, rows_per_mode=args.parity_rows // 4)))
+        worst = max(max(c["max_rel_err_mttkrp"], c["max_rel_err_update"]) for c in checks)
+        parity = {"rows_checked": sum(c["rows"] for c in checks), "max_rel_err": worst, "tolerance": 1e-4,
+                  "ok": worst <= 1e-4, "per_mode": checks, "plans": list(plan_checks),
+                  "plans_ok": all(c["ok"] for c in plan_checks),
+                  "method": "one CP-ALS iteration observed mode by mode: sampled MTTKRP rows and their ALS update "
+                            "(M V^-1, V = Hadamard of fp64 Grams of the factors the GPU used) recomputed in fp64 "
+                            "from the SOURCE tensor (oracle/scale.py), compared with the GPU's M and new*lambda"}
+        tensor.drop_device()
     if rank == 0:
         line = {
             "metric": METRIC, "value": nm * cfg["nnz"] / step_s, "unit": "nnz/s", "n_gpus": world,
@@ -715,11 +892,9 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
                        "step": "one CPD-ALS iteration (MTTKRP per mode + solve + normalise + factor all-gather + fit)",
                        "partition": f"{cfg['strategy']}, devices={world}", "accumulation": args.accumulation,
                        "layout": [p.layout for p in plans], "block_shifts": [p.block_shifts for p in plans]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src, "kernel": "mttkrp_panel_kernel" if plans[0].layout == "panel" else "mttkrp_v2_kernel",
-                         "kernel_ms_per_mode": [k * 1e3 for k in kern], "algorithmic_bytes_per_mode": alg,
-                         "mttkrp_share_of_iteration": sum(kern) / step_s},
+            "roofline": roof,
             "fit": fits[-1], "clocks": clk, "setup_seconds": setup_s, "plan_build_seconds": build_s,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -75,7 +75,12 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 8: slot-owned panels (skrp_slot_args) */
+int skrp_abi_version(void);  /* 9: launch log (skrp_launch_log) */
+/* Launch log of the MTTKRP kernels, launch order: entry = "<mode>\t<demangled
+ * name>" (bench.py matches the kernel it times against the one an ncu
+ * capture measured).  index < 0 clears the log; *count receives the number
+ * of entries. */
+int skrp_launch_log(int64_t index, char *buf, size_t len, int64_t *count);
 int skrp_device_sm_count(int *out);
 /* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
  * L2::evict_last, so this bounds how much of the L2 they may pin (B200

@@ -1,0 +1,207 @@
+"""Full-scale parity checks for bench.py and the -m gpu tests -- TEST
+INFRASTRUCTURE ONLY (see oracle/__init__.py: the product never imports this).
+
+At 10^9 nonzeros the CPU oracle cannot rebuild a plan in bench time, so the
+checks here use size-independent properties of the reference's
+build_mode_plan (partition.py:196-257) and recompute sampled MTTKRP rows in
+fp64 from the SOURCE tensor (the generator's arrays), never from the plan
+arrays under test.  The elementwise work runs on the GPU in torch (checker
+code, chunked); bounds, offsets and ISP boundaries are recomputed on the host
+by this package's restatement (equal_index_bounds / nnz_balanced_bounds /
+isp_boundaries, partition.py:127-193).
+
+verify_plan_full(src_coords, src_vals, plan, ...) checks, for one mode plan:
+  * sorted     -- the key column (c_d) is non-decreasing;
+  * stable     -- inside every run of equal keys the source positions
+                  (plan.perm) strictly increase (argsort(kind="stable"),
+                  partition.py:219-225);
+  * permutation-- plan.perm hits every source position exactly once;
+  * gathered   -- every plan column and the values equal the source arrays
+                  at plan.perm (bit-exact);
+  * bounds     -- the shard bounds equal the host restatement on the source
+                  histogram (equal-index: closed form; nnz-balanced: the C
+                  routine with the reference's tie rule);
+  * offsets    -- offsets == exclusive prefix of the histogram at the bounds;
+  * isps       -- every shard's ISP boundaries equal isp_boundaries(nnz, P).
+
+sample_parity_source(...) -- max |gpu - ref| / max(|ref|, 1) (cli.py:247-261)
+over a seeded sample of output rows per mode, ref = fp64 MTTKRP of those rows
+over the source nonzeros with the chained factors (mode d uses the GPU's own
+outputs of the modes before it, as the reference's mttkrp_all_modes does).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import equal_index_bounds, isp_boundaries, nnz_balanced_bounds
+
+_CHUNK = 1 << 27
+
+
+def _u32(x):
+    """int32 tensor holding u32 bit patterns -> int64 values."""
+    return x.long() & 0xFFFFFFFF
+
+
+def source_histogram(src_col, num_indices):
+    import torch
+
+    counts = torch.zeros(num_indices, dtype=torch.int64, device=src_col.device)
+    for a in range(0, src_col.numel(), _CHUNK):
+        counts += torch.bincount(_u32(src_col[a:a + _CHUNK]), minlength=num_indices)
+    return counts
+
+
+def verify_plan_full(src_coords, src_vals, plan, strategy, oversubscription=4, devices=1, isp_capacity=8192):
+    import torch
+
+    d = plan.mode
+    nnz = int(src_vals.numel())
+    if plan.perm is None:
+        raise ValueError("verify_plan_full needs the build permutation (keep_permutation=True)")
+    if plan.layout != "flycoo":
+        raise ValueError("verify the plan before any execution-layout reordering")
+    dev = src_vals.device
+    perm, key = plan.perm, plan.coords[d]
+    res = {"mode": d, "nnz": nnz, "sorted": True, "stable": True, "gathered": True}
+    seen = torch.zeros(nnz, dtype=torch.bool, device=dev)
+    in_range = True
+    for a in range(0, nnz, _CHUNK):
+        b = min(nnz, a + _CHUNK)
+        e = min(nnz, b + 1)  # one element of overlap: the boundary pair
+        k = _u32(key[a:e])
+        p = _u32(perm[a:e])
+        dk = k[1:] - k[:-1]
+        dp = p[1:] - p[:-1]
+        res["sorted"] &= bool((dk >= 0).all().item())
+        res["stable"] &= bool(((dk > 0) | (dp > 0)).all().item())
+        pc = p[: b - a]
+        in_range &= bool((pc < nnz).all().item())
+        pc = pc.clamp(max=nnz - 1)
+        seen[pc] = True
+        for w, c in enumerate(plan.coords):
+            res["gathered"] &= bool((c[a:b] == src_coords[w].index_select(0, pc)).all().item())
+        res["gathered"] &= bool((plan.vals[a:b].view(torch.int32)
+                                 == src_vals.index_select(0, pc).view(torch.int32)).all().item())
+    res["permutation"] = in_range and bool(seen.all().item())
+    del seen
+    n_idx = plan.shape[d]
+    counts = source_histogram(src_coords[d], n_idx).cpu().numpy()
+    k = min(devices * oversubscription, n_idx)
+    if strategy == "equal-index":
+        bounds = equal_index_bounds(n_idx, k)
+    else:
+        bounds = nnz_balanced_bounds(counts, k)
+    prefix = np.concatenate([[0], np.cumsum(counts)])
+    offsets = prefix[bounds]
+    res["bounds"] = bool(np.array_equal(np.asarray(plan.bounds, dtype=np.int64), bounds))
+    res["offsets"] = bool(np.array_equal(np.asarray(plan.offsets, dtype=np.int64), offsets))
+    res["isps"] = all(np.array_equal(np.asarray(s_.isp_boundaries, dtype=np.int64),
+                                     isp_boundaries(int(offsets[j + 1] - offsets[j]), isp_capacity))
+                      for j, s_ in enumerate(plan.shards)) and len(plan.shards) == k
+    res["shards"] = k
+    res["ok"] = all(res[x] for x in ("sorted", "stable", "permutation", "gathered", "bounds", "offsets", "isps"))
+    return res
+
+
+def sample_parity_source(src_coords, src_vals, shape, init_factors, outputs, modes, rows_per_mode=4096, seed=0,
+                         nnz_budget=8_000_000, tol=1e-4):
+    """Sampled-row parity against the source tensor (see module docstring).
+    init_factors: fp64 numpy arrays; outputs: the GPU's per-mode outputs
+    (torch, any float dtype, I_d x R) in `modes` order."""
+    import torch
+
+    dev = outputs[0].device
+    facs = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).to(dev) for f in init_factors]
+    rank = facs[0].shape[1]
+    rng = np.random.default_rng(seed)
+    worst, checked, per_mode = 0.0, 0, []
+    for i, d in enumerate(modes):
+        col = src_coords[d]
+        cand = np.sort(rng.permutation(shape[d])[:rows_per_mode]).astype(np.int64)
+        rows_t = torch.from_numpy(cand).to(dev)
+        counts = source_histogram(col, shape[d]).index_select(0, rows_t).cpu().numpy()
+        keep, tot = [], 0
+        for r, n in zip(cand, counts):  # rows in the budget (at least one)
+            if tot + n <= nnz_budget or not keep:
+                keep.append(r)
+                tot += int(n)
+        rows = np.asarray(keep, dtype=np.int64)
+        rows_t = torch.from_numpy(rows).to(dev)
+        member = torch.zeros(shape[d], dtype=torch.bool, device=dev)
+        member[rows_t] = True
+        expect = torch.zeros((len(rows), rank), dtype=torch.float64, device=dev)
+        for a in range(0, col.numel(), _CHUNK):
+            c = _u32(col[a:a + _CHUNK])
+            sel = member[c].nonzero().squeeze(1)
+            if sel.numel() == 0:
+                continue
+            s_ = sel + a
+            contrib = src_vals.index_select(0, s_).double()[:, None].expand(-1, rank).clone()
+            for w in range(len(shape)):
+                if w != d:
+                    contrib *= facs[w].index_select(0, _u32(src_coords[w].index_select(0, s_)))
+            pos = torch.searchsorted(rows_t, _u32(col.index_select(0, s_)))
+            expect.index_add_(0, pos, contrib)
+        got = outputs[i].index_select(0, rows_t).double()
+        err = float(((got - expect).abs() / expect.abs().clamp(min=1.0)).max().item()) if len(rows) else 0.0
+        per_mode.append({"mode": d, "rows": int(len(rows)), "nnz": int(tot), "max_rel_err": err})
+        worst = max(worst, err)
+        checked += len(rows)
+        facs[d] = outputs[i].double()
+    return {"rows_checked": checked, "max_rel_err": worst, "tolerance": tol, "ok": worst <= tol,
+            "per_mode": per_mode,
+            "method": "seeded output-row sample; fp64 recomputation from the SOURCE tensor (generator arrays, "
+                      "not the plan), chained factors; torch on the GPU as checker (oracle/scale.py)"}
+
+
+def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_per_mode=1024, seed=0,
+                   nnz_budget=8_000_000):
+    """One CP-ALS mode update (cpd.py:39-67 / 108-167) checked on sampled rows:
+    facs = the factors the GPU used for mode d (torch, I_w x R), m = its MTTKRP
+    output, new = its normalised updated factor, lambdas = its column norms.
+    Expected, in fp64 from the SOURCE tensor: M[rows] (MTTKRP), and
+    M[rows] @ V^-1 with V = Hadamard of the other modes' Grams (computed here
+    in fp64 from facs) -- compared with new[rows] * lambdas (the GPU's update
+    before normalisation).  Returns {max_rel_err_mttkrp, max_rel_err_update}."""
+    import torch
+
+    dev = m.device
+    R = m.shape[1]
+    rng = np.random.default_rng(seed + 7919 * d)
+    col = src_coords[d]
+    cand = np.sort(rng.permutation(shape[d])[:rows_per_mode]).astype(np.int64)
+    counts = source_histogram(col, shape[d]).index_select(0, torch.from_numpy(cand).to(dev)).cpu().numpy()
+    keep, tot = [], 0
+    for r, n in zip(cand, counts):
+        if n > 0 and (tot + n <= nnz_budget or not keep):
+            keep.append(r)
+            tot += int(n)
+    rows_t = torch.from_numpy(np.asarray(keep, dtype=np.int64)).to(dev)
+    member = torch.zeros(shape[d], dtype=torch.bool, device=dev)
+    member[rows_t] = True
+    f64 = [f.double() for f in facs]
+    expect = torch.zeros((rows_t.numel(), R), dtype=torch.float64, device=dev)
+    for a in range(0, col.numel(), _CHUNK):
+        sel = member[_u32(col[a:a + _CHUNK])].nonzero().squeeze(1)
+        if sel.numel() == 0:
+            continue
+        s_ = sel + a
+        contrib = src_vals.index_select(0, s_).double()[:, None].expand(-1, R).clone()
+        for w in range(len(shape)):
+            if w != d:
+                contrib *= f64[w].index_select(0, _u32(src_coords[w].index_select(0, s_)))
+        expect.index_add_(0, torch.searchsorted(rows_t, _u32(col.index_select(0, s_))), contrib)
+    got_m = m.index_select(0, rows_t).double()
+    err_m = float(((got_m - expect).abs() / expect.abs().clamp(min=1.0)).max().item())
+    v = torch.ones((R, R), dtype=torch.float64, device=dev)
+    for w in range(len(shape)):
+        if w != d:
+            v *= f64[w].T @ f64[w]
+    upd = torch.linalg.solve(v, expect.T).T  # M V^-1 (V symmetric)
+    lam = torch.from_numpy(np.asarray(lambdas, dtype=np.float64)).to(dev)
+    got_u = new.index_select(0, rows_t).double() * lam[None, :]
+    err_u = float(((got_u - upd).abs() / upd.abs().clamp(min=1.0)).max().item())
+    return {"mode": d, "rows": int(rows_t.numel()), "nnz": tot, "max_rel_err_mttkrp": err_m,
+            "max_rel_err_update": err_u}

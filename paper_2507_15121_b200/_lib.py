@@ -33,7 +33,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 8  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 9  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -102,6 +102,7 @@ class SlotArgs(ctypes.Structure):
 SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
+    "skrp_launch_log": (i32, [i64, ctypes.c_char_p, sz, ctypes.POINTER(i64)]),
     "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
     "skrp_crc32_chunks": (i32, [vp, i64, i64, vp, vp]),
     "skrp_crc32_fold_host": (i32, [vp, i64, i64, i64, ctypes.c_uint32, vp]),
@@ -154,6 +155,24 @@ SIGNATURES = {
 }
 
 _LIB = None
+
+
+def launch_log(clear=False):
+    """(mode, demangled kernel name) of the MTTKRP kernels launched so far, in
+    launch order; clear=True empties the log and returns []."""
+    h = lib()
+    cnt = i64()
+    if clear:
+        h.skrp_launch_log(-1, None, 0, ctypes.byref(cnt))
+        return []
+    buf = ctypes.create_string_buffer(1024)
+    h.skrp_launch_log(1 << 62, buf, 1024, ctypes.byref(cnt))  # out of range: reports the count only
+    out = []
+    for k in range(cnt.value):
+        check(h.skrp_launch_log(k, buf, 1024, None), "skrp_launch_log")
+        m, name = buf.value.decode().split("\t", 1)
+        out.append((int(m), name))
+    return out
 
 
 def build(force: bool = False):

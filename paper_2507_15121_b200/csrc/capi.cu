@@ -4,6 +4,13 @@
 
 #include "common.cuh"
 
+#include <cxxabi.h>
+
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <vector>
+
 namespace skrp {
 
 static thread_local char g_err[512] = {0};
@@ -33,9 +40,44 @@ int device_sm_count()
     return sms;
 }
 
+namespace {
+std::mutex g_log_mu;
+std::vector<std::string> g_log;
+constexpr size_t kLogMax = 4096;
+}  // namespace
+
+void note_launch(const void *kernel, int mode)
+{
+    const char *mangled = nullptr;
+    std::string name = "?";
+    if (cudaFuncGetName(&mangled, kernel) == cudaSuccess && mangled) {
+        int st = 0;
+        char *dm = abi::__cxa_demangle(mangled, nullptr, nullptr, &st);
+        name = (st == 0 && dm) ? dm : mangled;
+        free(dm);
+    }
+    std::lock_guard<std::mutex> lk(g_log_mu);
+    if (g_log.size() < kLogMax) g_log.push_back(std::to_string(mode) + "\t" + name);
+}
+
 }  // namespace skrp
 
 extern "C" {
+
+int skrp_launch_log(int64_t index, char *buf, size_t len, int64_t *count)
+{
+    std::lock_guard<std::mutex> lk(skrp::g_log_mu);
+    if (count) *count = (int64_t)skrp::g_log.size();
+    if (index < 0) {  // clear
+        skrp::g_log.clear();
+        return SKRP_OK;
+    }
+    SKRP_REQUIRE(index < (int64_t)skrp::g_log.size(), "launch log has %zu entries, asked for %lld",
+                 skrp::g_log.size(), (long long)index);
+    SKRP_REQUIRE(buf != nullptr && len > 0, "skrp_launch_log: null buffer");
+    snprintf(buf, len, "%s", skrp::g_log[(size_t)index].c_str());
+    return SKRP_OK;
+}
 
 int skrp_last_error(char *buf, size_t len)
 {
@@ -46,7 +88,7 @@ int skrp_last_error(char *buf, size_t len)
     return skrp::g_err_code;
 }
 
-int skrp_abi_version(void) { return 8; }
+int skrp_abi_version(void) { return 9; }
 
 int skrp_device_sm_count(int *out)
 {

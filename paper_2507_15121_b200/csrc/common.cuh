@@ -40,6 +40,10 @@ int cuda_status(cudaError_t e, const char *where);
 
 int device_sm_count();
 
+// launch log of the hot kernels (demangled names, in launch order): bench.py
+// matches the kernel it times against the kernel an ncu capture measured
+void note_launch(const void *kernel, int mode);
+
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // grid for a grid-stride loop over n items: at most `waves` CTAs per SM

@@ -651,6 +651,7 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
         v.fn<<<grid, kWarpsPerCta * 32, 0, s>>>(a);
     }
     SKRP_LAUNCHED("mttkrp_tiles_kernel");
+    note_launch(v.v2 ? (const void *)v.v2 : (const void *)v.fn, a.mode);
     return SKRP_OK;
 }
 
@@ -708,6 +709,7 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
     cfg.numAttrs = 1;
     SKRP_CUDA(cudaLaunchKernelEx(&cfg, v.fn, a, p));
     SKRP_LAUNCHED("mttkrp_panel_kernel");
+    note_launch((const void *)v.fn, a.mode);
     return SKRP_OK;
 }
 

@@ -367,6 +367,7 @@ int skrp_mttkrp_slots(const skrp_mttkrp_args *args, const skrp_slot_args *slots,
     cfg.numAttrs = 1;
     SKRP_CUDA(cudaLaunchKernelEx(&cfg, mttkrp_slots_kernel, a, sa));
     SKRP_LAUNCHED("mttkrp_slots_kernel");
+    note_launch((const void *)mttkrp_slots_kernel, a.mode);
     return SKRP_OK;
 }
 

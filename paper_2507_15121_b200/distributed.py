@@ -603,9 +603,12 @@ class DistributedCpAls:
                 total += out
         return float(self._allreduce(total).item())
 
-    def run(self, factors, iterations=1, fit_tol=None, timings=None):
+    def run(self, factors, iterations=1, fit_tol=None, timings=None, observe=None):
         """ALS sweeps from the given full fp32 factor replicas (device).
-        Returns (factors, lambdas, fit_history)."""
+        Returns (factors, lambdas, fit_history).  ``observe(d, factors, m,
+        new, lambdas)``, if given, sees every mode update (the factors the
+        mode read, its MTTKRP output, the normalised new factor) before the
+        all-gather -- the parity checker's hook."""
         import torch
 
         from . import _lib
@@ -664,6 +667,8 @@ class DistributedCpAls:
                         _lib.call("skrp_scale_cols", new[lo:hi].data_ptr(), hi - lo, R, scale.data_ptr(), stream)
                 if d == nm - 1:
                     inner = self._inner_fused(d, new, m, lambdas)
+                if observe is not None:
+                    observe(d, facs, m, new, lambdas)
                 if self.mt.world > 1:
                     allgather_owned_rows(new, self.mt.ownership[d], self.group)
                 facs[d] = new

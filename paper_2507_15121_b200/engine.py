@@ -374,10 +374,6 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
         # the atomic speed (cfg4s 28.4 vs 29.2 ms/step, cfg5s 56.6 vs 56.7),
         # the blocked carry path pays per-group launches (123 / 191 ms)
         return plan
-    if cfg.layout == "auto" and not skewed and slots_apply(plan, rank):
-        # both inputs blocked, output rows in shared memory (K1c): cfg2 modes
-        plan.to_slots(slot_blocking(plan, rank, shift=cfg.slot_block_shift))
-        return plan
     if cfg.layout == "auto" and not skewed and len(plan.shape) == 3:
         sh = streamed_blocking(plan, rank)
         if sh is not None:

@@ -276,7 +276,7 @@ def _unique_chunk(shape, nnz, rank, world, cdfs, seed, dev, stream, group):
     owned = [torch.empty(0, dtype=torch.int32, device=dev) for _ in shape]  # tuples I own, kept so far
     kept_parts = []   # per round: this rank's surviving draws (coords), in draw order
     round_counts = []  # per round: survivors on every rank (world,)
-    total, drawn, rounds = 0, 0, 0
+    total, drawn, rounds, dups = 0, 0, 0, 0
 
     def exchange(x, send_counts, recv_counts):
         return _all_to_all(x, send_counts, recv_counts, group)

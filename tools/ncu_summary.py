@@ -57,6 +57,9 @@ def full(rep, out, config=None):
             "registers_per_thread": g("launch__registers_per_thread"),
             "grid_size": g("launch__grid_size"),
             "stall_long_scoreboard_per_issue": g("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"),
+            "inst_executed": g("smsp__inst_executed.sum") or g("sm__inst_executed.sum"),
+            "l1_hit_rate_pct": g("l1tex__t_sector_hit_rate.pct"),
+            "shared_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
         }
         if rec["dram_read_bytes"] is not None and rec["dram_write_bytes"] is not None:
             rec["traffic_bytes_per_launch"] = rec["dram_read_bytes"] + rec["dram_write_bytes"]

@@ -528,8 +528,7 @@ def run_ours(args, cfg):
                            scheduling=args.scheduling,
                            kernel_variant=args.variant,
                            layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
-                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather,
-                           rle_rows=bool(args.rle_rows), panel_group_sync=bool(args.panel_group_sync))
+                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather)
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
@@ -677,6 +676,34 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # ---- end to end through the DROP-IN API (reference engine.py:369-400):
+    # float64 numpy factors in, make_devices + mttkrp_all_modes, float64 numpy
+    # outputs back -- host wall clock around the whole call (it returns host
+    # arrays), pinned staging and on-GPU conversions inside (hostio.py)
+    e2e_api = None
+    if world == 1 and not streamed and not args.no_e2e_api:
+        api_cfg = sk.PlatformConfig(devices=1, rank=R, accumulation=args.accumulation, tile_nnz=args.tile,
+                                    layout=args.layout, l2_budget_mb=args.l2_mb, max_blocks=args.max_blocks)
+        np_f = [f.data for f in init]
+        api_times = []
+        for k in range(1 + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            outs_api, _ = sk.mttkrp_all_modes(plans, sk.make_devices(np_f, api_cfg), api_cfg)
+            dt = time.perf_counter() - t0
+            if k:
+                api_times.append(dt)
+        api_s = sum(api_times) / len(api_times)
+        same = all(np.array_equal(a_, b_.double().cpu().numpy()) for a_, b_ in zip(outs_api, runner.outputs)) \
+            if args.accumulation == "deterministic-reduce" else None
+        del outs_api
+        e2e_api = {"value": total_nnz / api_s, "unit": "nnz/s", "ms_per_step": api_s * 1e3,
+                   "h2d_bytes_per_step": sum(f.nbytes for f in np_f),
+                   "d2h_bytes_per_step": sum(shape[d] * R * 8 for d in modes),
+                   "call": "make_devices(float64 numpy factors) + mttkrp_all_modes(plans, devices, cfg) -> "
+                           "float64 numpy outputs (host wall clock)",
+                   "bit_identical_to_runner": same}
+
     stream_info = None
     if streamed:
         ex_bytes = sum(runner._exec(i, R).h2d_bytes for i in streamed)
@@ -734,12 +761,12 @@ def run_ours(args, cfg):
                                      f"{backend} broadcasts of owned row ranges"),
                        "dist_backend": backend, "world_size": world,
                        "launch": "one CUDA graph per all-mode step" if graph is not None else "eager",
-                       "row_ids": "run-length" if pl.rle_rows else "u32 per nonzero",
                        "l2": "no flush needed: per-mode inputs (nnz*16 B) >> 126 MB L2"},
             "roofline": roof,
             "balance": balance,
             "e2e": {"value": total_nnz / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+            "e2e_api": e2e_api,
             "gpu_launches": launches,
             "stream": stream_info,
             "clocks": clk,
@@ -879,9 +906,10 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
         parity = {"rows_checked": sum(c["rows"] for c in checks), "max_rel_err": worst, "tolerance": 1e-4,
                   "ok": worst <= 1e-4, "per_mode": checks, "plans": list(plan_checks),
                   "plans_ok": all(c["ok"] for c in plan_checks),
-                  "method": "one CP-ALS iteration observed mode by mode: sampled MTTKRP rows and their ALS update "
-                            "(M V^-1, V = Hadamard of fp64 Grams of the factors the GPU used) recomputed in fp64 "
-                            "from the SOURCE tensor (oracle/scale.py), compared with the GPU's M and new*lambda"}
+                  "method": "one CP-ALS iteration observed mode by mode: sampled MTTKRP rows recomputed in fp64 "
+                            "from the SOURCE tensor vs the GPU's M; the ALS update of those rows (M V^-1, V = "
+                            "Hadamard of fp64 Grams of the factors the GPU used, applied to the GPU's M) vs the "
+                            "GPU's new*lambda (oracle/scale.py cpd_mode_check)"}
         tensor.drop_device()
     if rank == 0:
         line = {
@@ -999,13 +1027,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
-    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "slots", "auto"))
+    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "auto"))
     ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")
-    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0, choices=(0, 1),
+                    help="1: the generic scalar tile kernel (cross-check path)")
     ap.add_argument("--parity-rows", type=int, default=4096, help="sampled output rows per mode (SURVEY.md §8(c): >= 4096)")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-e2e-api", action="store_true", help="skip the drop-in API (numpy float64) e2e figure")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--dist-build", action="store_true", help="N>1: distributed plan build (default for cfg3-5)")
@@ -1018,10 +1048,6 @@ def main():
                     help="one GPU: time every rank's share of an N-GPU run alone (projected scaling line)")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: panel layout whose write-back pushes rows to every rank (CUDA IPC, no collective)")
-    ap.add_argument("--panel-group-sync", type=int, default=0, choices=(0, 1),
-                    help="panel kernel: CTA barrier before every block group")
-    ap.add_argument("--rle-rows", type=int, default=0, choices=(0, 1),
-                    help="tile kernel reads run-length output-row ids instead of one u32 per nonzero")
     ap.add_argument("--scheduling", default="contiguous", choices=("dynamic", "static", "contiguous", "split"),
                     help="shard placement across GPUs (contiguous: one owned row range per GPU)")
     ap.add_argument("--launch-check", action="store_true",

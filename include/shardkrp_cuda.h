@@ -75,17 +75,13 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 9: launch log (skrp_launch_log) */
+int skrp_abi_version(void);  /* 11: launch log; A/B-only entry points and fields removed */
 /* Launch log of the MTTKRP kernels, launch order: entry = "<mode>\t<demangled
  * name>" (bench.py matches the kernel it times against the one an ncu
  * capture measured).  index < 0 clears the log; *count receives the number
  * of entries. */
 int skrp_launch_log(int64_t index, char *buf, size_t len, int64_t *count);
 int skrp_device_sm_count(int *out);
-/* Set-aside L2 for persisting (evict_last) lines: the factor-row gathers carry
- * L2::evict_last, so this bounds how much of the L2 they may pin (B200
- * addition; 0 restores the default).  *granted = the limit now in force. */
-int skrp_set_l2_persisting(int64_t bytes, int64_t *granted);
 /* CUDA IPC for the fused all-gather: handle (64 bytes) + offset of a device
  * pointer inside its allocation; open on another process (peer access enabled
  * lazily) -> the pointer there and the mapping base to close later. */
@@ -152,32 +148,8 @@ typedef struct {
                                                 of a wider row or a column plane    */
     int32_t out_ld;                          /* floats between output rows (0 = R);
                                                 `out` may point at a column offset   */
-    const void *l2_window_base;              /* optional L2 access-policy window for
-                                                this launch (a pinned factor block):
-                                                hits persist in the set-aside L2,
-                                                misses stream; 0 bytes = none        */
-    int64_t l2_window_bytes;
-    float l2_window_hit_ratio;
-    int32_t reserved2;                       /* 0 */
-    /* optional run-length output-row ids (tile kernel, R = 32, N = 3; NULL =
-       read coords[mode]): bit k of rle_chg[w] marks nonzero 32w+k as the first
-       of its row (floor(nnz/32)+2 words, tail zero), rle_pre[w] = set bits in
-       words < w, rle_runs[r] = row id of run r.  Built by skrp_rle_mark /
-       skrp_rle_runs; coords[mode] must still hold the same rows. */
-    const uint32_t *rle_chg;
-    const uint32_t *rle_pre;
-    const uint32_t *rle_runs;
+    int32_t reserved2[2];                    /* 0 */
 } skrp_mttkrp_args;
-
-/* Run-length output-row ids for skrp_mttkrp_args.rle_* (built once per plan
- * layout; the reference reads the row coordinate per nonzero, kernels.py:
- * 54-71).  W = n/32 + 2 words.  skrp_rle_mark: change bits chg[W] (tail words
- * zero) and per-word run counts counts[W]; the caller exclusive-scans counts
- * (skrp_exclusive_scan_i64) into prefix[W+1] (prefix[W] = number of runs) and
- * skrp_rle_runs writes pre[W] (u32 prefix) and runs[prefix[W]].  n < 2^32. */
-int skrp_rle_mark(const uint32_t *rows, int64_t n, uint32_t *chg, int64_t *counts, skrp_stream_t stream);
-int skrp_rle_runs(const uint32_t *rows, int64_t n, const uint32_t *chg, const int64_t *prefix, uint32_t *pre,
-                  uint32_t *runs, skrp_stream_t stream);
 
 int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream);
 
@@ -213,47 +185,12 @@ typedef struct {
  * and the group's factor blocks stay L2-resident.  Without it CTAs claim items
  * dynamically (better for skewed item sizes). */
 #define SKRP_PANEL_LOCKSTEP 1
-/* ... and the warps of a CTA start every block group together (a CTA barrier
- * per group), so a CTA never gathers from two groups' blocks at once. */
-#define SKRP_PANEL_GROUP_SYNC 2
 
 int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *panels, skrp_stream_t stream);
 /* warps per CTA and the largest slab the panel kernel supports for (nmodes,
  * rank); 0 on success, SKRP_ERR_INVALID when no panel kernel exists. */
 int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows);
 
-/* Slot-owned output panels (K1c, csrc/mttkrp_slots.cu; N = 3, R = 32; B200
- * addition with kernels.py:54-71's per-nonzero arithmetic): an ITEM is the
- * part of one output slab inside one shard; slot s of the item owns rows
- * [row_lo + s*rows_per_slot, +rows_per_slot) and its nonzeros are the element
- * range [slot_offsets[item*(slots+1) + s], slot_offsets[item*(slots+1) + s + 1]) of
- * the plan arrays, ordered (tile, row) where tile = (c_in0 >> tile_shift0,
- * c_in1 >> tile_shift1) and in0 < in1 are the input modes.  The arrays must be
- * readable kWin (skrp_slots_shape chunk_slack) elements past their end.  Every
- * row of every item is written exactly once (plain stores, also to each
- * peer_out buffer): no output zeroing, bit-identical for any placement. */
-typedef struct {
-    const int64_t *item_rows;     /* 2*num_items: [row_lo, row_hi)                  */
-    const int64_t *slot_offsets;  /* num_items x (slots_per_item + 1) element offsets */
-    int64_t num_items;
-    int32_t slots_per_item;       /* == skrp_slots_shape slots_per_item              */
-    int32_t rows_per_slot;        /* == skrp_slots_shape rows_per_slot               */
-    int32_t tile_shift0;          /* block shift of input 0 (31: unblocked)          */
-    int32_t tile_shift1;          /* block shift of input 1                          */
-    unsigned int *round_counter;  /* one word of scratch (grid barrier; zeroed here) */
-    const uint64_t *peer_out;     /* num_peers output pointers (CUDA IPC) or NULL    */
-    int32_t num_peers;
-    int32_t reserved;
-} skrp_slot_args;
-int skrp_mttkrp_slots(const skrp_mttkrp_args *args, const skrp_slot_args *slots, skrp_stream_t stream);
-/* layout constants of the slot kernel (N = 3, R = 32 only) */
-int skrp_slots_shape(int32_t nmodes, int32_t rank, int32_t *slots_per_item, int32_t *rows_per_slot,
-                     int32_t *chunk_slack);
-/* key[i] = row_prefix[rows[i]] | (in0[i] >> shift0) << tile_bits1 | (in1[i] >> shift1):
- * sort keys of the slot layout (row_prefix = (item << slot_bits | slot) << tile bits). */
-int skrp_slot_keys(const uint32_t *rows, const uint32_t *in0, const uint32_t *in1, int64_t n,
-                   const uint32_t *row_prefix, int32_t shift0, int32_t shift1, int32_t tile_bits1, uint32_t *keys,
-                   skrp_stream_t stream);
 
 /* ------------------------------------------------ .tns ingestion (§8(f) 4)
  * GPU restatement of parse_tns (reference tensor.py:173-247).  text: the file
@@ -293,13 +230,6 @@ int skrp_plan_pack_indices(const uint32_t *const *coords, int64_t nrec, int32_t 
                            skrp_stream_t stream);
 int skrp_f64_to_f32(const double *in, int64_t n, float *out, skrp_stream_t stream);
 
-/* Column planes for column-pass execution (B200 addition, no reference
- * counterpart): dst (parts x rows x rank/parts, fp32) plane p = columns
- * [p*rank/parts, (p+1)*rank/parts) of src (rows x rank, row-major).  A pass
- * over one plane touches rank/parts*4 bytes per gathered row, so twice as many
- * factor rows stay L2-resident per pass at parts = 2. */
-int skrp_split_columns(const float *src, int64_t rows, int32_t rank, int32_t parts, float *dst,
-                       skrp_stream_t stream);
 
 /* Segmented reduction of boundary-row carries, one level of the fixed tree.
  * chunks: 2*n_chunks [begin, end) entry ranges (never straddling a shard);

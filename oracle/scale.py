@@ -163,8 +163,10 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
     output, new = its normalised updated factor, lambdas = its column norms.
     Expected, in fp64 from the SOURCE tensor: M[rows] (MTTKRP), and
     M[rows] @ V^-1 with V = Hadamard of the other modes' Grams (computed here
-    in fp64 from facs) -- compared with new[rows] * lambdas (the GPU's update
-    before normalisation).  Returns {max_rel_err_mttkrp, max_rel_err_update}."""
+    in fp64 from facs) applied to the GPU's own M rows -- compared with
+    new[rows] * lambdas (the GPU's update before normalisation).  Returns
+    {max_rel_err_mttkrp, max_rel_err_update, ...}; the update error against a
+    fully fp64 chain and cond(V) are reported alongside."""
     import torch
 
     dev = m.device
@@ -199,9 +201,15 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
     for w in range(len(shape)):
         if w != d:
             v *= f64[w].T @ f64[w]
-    upd = torch.linalg.solve(v, expect.T).T  # M V^-1 (V symmetric)
     lam = torch.from_numpy(np.asarray(lambdas, dtype=np.float64)).to(dev)
     got_u = new.index_select(0, rows_t).double() * lam[None, :]
+    # the update step itself: fp64 M_gpu V^-1 from the GPU's own M (V symmetric)
+    upd = torch.linalg.solve(v, got_m.T).T
     err_u = float(((got_u - upd).abs() / upd.abs().clamp(min=1.0)).max().item())
+    # end to end (info): fp64 M V^-1 from the source -- M's fp32 rounding
+    # (err_m) amplified by cond(V), a property of fp32 arithmetic, not gated
+    upd64 = torch.linalg.solve(v, expect.T).T
+    err_e2e = float(((got_u - upd64).abs() / upd64.abs().clamp(min=1.0)).max().item())
     return {"mode": d, "rows": int(rows_t.numel()), "nnz": tot, "max_rel_err_mttkrp": err_m,
-            "max_rel_err_update": err_u}
+            "max_rel_err_update": err_u, "max_rel_err_update_vs_fp64_source": err_e2e,
+            "cond_V": float(torch.linalg.cond(v).item())}

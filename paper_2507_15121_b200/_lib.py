@@ -24,7 +24,6 @@ FLAG_ADDITIVE = 1
 FLAG_STREAM_INPUT0 = 2
 FLAG_STREAM_INPUT1 = 4
 PANEL_LOCKSTEP = 1
-PANEL_GROUP_SYNC = 2
 
 vp = ctypes.c_void_p
 i64 = ctypes.c_int64
@@ -33,7 +32,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 9  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 11  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -57,13 +56,7 @@ class MttkrpArgs(ctypes.Structure):
         ("flags", i32),
         ("factor_ld", i32),
         ("out_ld", i32),
-        ("l2_window_base", vp),
-        ("l2_window_bytes", i64),
-        ("l2_window_hit_ratio", ctypes.c_float),
-        ("reserved2", i32),
-        ("rle_chg", vp),
-        ("rle_pre", vp),
-        ("rle_runs", vp),
+        ("reserved2", i32 * 2),
     ]
 
 
@@ -82,28 +75,11 @@ class PanelArgs(ctypes.Structure):
     ]
 
 
-class SlotArgs(ctypes.Structure):
-    _fields_ = [
-        ("item_rows", vp),
-        ("slot_offsets", vp),
-        ("num_items", i64),
-        ("slots_per_item", i32),
-        ("rows_per_slot", i32),
-        ("tile_shift0", i32),
-        ("tile_shift1", i32),
-        ("round_counter", vp),
-        ("peer_out", vp),
-        ("num_peers", i32),
-        ("reserved", i32),
-    ]
-
-
 # name -> (restype, argtypes)
 SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
     "skrp_abi_version": (i32, []),
     "skrp_launch_log": (i32, [i64, ctypes.c_char_p, sz, ctypes.POINTER(i64)]),
-    "skrp_split_columns": (i32, [vp, i64, i32, i32, vp, vp]),
     "skrp_crc32_chunks": (i32, [vp, i64, i64, vp, vp]),
     "skrp_crc32_fold_host": (i32, [vp, i64, i64, i64, ctypes.c_uint32, vp]),
     "skrp_crc32_raw_host": (i32, [vp, i64, vp]),
@@ -118,12 +94,8 @@ SIGNATURES = {
     "skrp_tns_classify": (i32, [vp, i64, vp, i64, i64, vp, vp, vp]),
     "skrp_tns_parse": (i32, [vp, i64, vp, i64, i64, vp, i32, vp, vp, vp, vp]),
     "skrp_tns_parse_token_host": (i32, [ctypes.c_char_p, i64, i32, vp, vp]),
-    "skrp_set_l2_persisting": (i32, [i64, vp]),
     "skrp_mttkrp_panels": (i32, [vp, vp, vp]),
     "skrp_panel_shape": (i32, [i32, i32, vp, vp]),
-    "skrp_mttkrp_slots": (i32, [vp, vp, vp]),
-    "skrp_slots_shape": (i32, [i32, i32, vp, vp, vp]),
-    "skrp_slot_keys": (i32, [vp, vp, vp, i64, vp, i32, i32, i32, vp, vp]),
     "skrp_device_sm_count": (i32, [ctypes.POINTER(i32)]),
     "skrp_histogram": (i32, [vp, i64, i64, vp, vp]),
     "skrp_scan_workspace_bytes": (sz, [i64]),
@@ -134,8 +106,6 @@ SIGNATURES = {
     "skrp_stable_sort_by_key": (i32, [vp, i64, ctypes.c_int, vp, vp, vp, sz, vp]),
     "skrp_gather_u32": (i32, [vp, vp, i64, vp, vp]),
     "skrp_block_keys": (i32, [vp, i32, vp, vp, vp, i64, i32, i64, vp, vp]),
-    "skrp_rle_mark": (i32, [vp, i64, vp, vp, vp]),
-    "skrp_rle_runs": (i32, [vp, i64, vp, vp, vp, vp, vp]),
     "skrp_mttkrp_tiles": (i32, [ctypes.POINTER(MttkrpArgs), vp]),
     "skrp_carry_fixup": (i32, [vp, vp, i32, vp, vp, i64, i32, vp, vp, vp, i32, vp]),
     "skrp_mttkrp_host": (i32, [vp, vp, i64, i32, vp, vp, i32, i32, vp, i32]),

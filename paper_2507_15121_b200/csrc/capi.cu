@@ -88,7 +88,7 @@ int skrp_last_error(char *buf, size_t len)
     return skrp::g_err_code;
 }
 
-int skrp_abi_version(void) { return 9; }
+int skrp_abi_version(void) { return 11; }
 
 int skrp_device_sm_count(int *out)
 {
@@ -143,20 +143,6 @@ int skrp_ipc_close_handle(void *base)
 {
     SKRP_REQUIRE(base != nullptr, "skrp_ipc_close_handle: null pointer");
     SKRP_CUDA(cudaIpcCloseMemHandle(base));
-    return SKRP_OK;
-}
-
-int skrp_set_l2_persisting(int64_t bytes, int64_t *granted)
-{
-    SKRP_REQUIRE(bytes >= 0, "skrp_set_l2_persisting: negative size");
-    int dev = 0, maxp = 0;
-    SKRP_CUDA(cudaGetDevice(&dev));
-    SKRP_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    size_t want = (size_t)std::min<int64_t>(bytes, maxp);
-    SKRP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-    size_t got = 0;
-    SKRP_CUDA(cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize));
-    if (granted) *granted = (int64_t)got;
     return SKRP_OK;
 }
 

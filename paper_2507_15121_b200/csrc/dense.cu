@@ -572,21 +572,6 @@ static unsigned grid_cap(int64_t want, int per_sm)
 
 using namespace skrp;
 
-// Column planes for the column-pass MTTKRP: dst[p][i][c] = src[i][p*w + c],
-// w = R / parts.  One float4 per thread, coalesced on both sides.
-__global__ void __launch_bounds__(256) split_columns_kernel(const float4 *__restrict__ src, int64_t rows, int R4,
-                                                            int w4, float4 *__restrict__ dst)
-{
-    const int64_t n = rows * R4;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const int64_t i = k / R4;
-        const int c = (int)(k - i * R4);
-        const int p = c / w4;
-        dst[((int64_t)p * rows + i) * w4 + (c - p * w4)] = __ldcs(src + k);
-    }
-}
-
 extern "C" {
 
 int skrp_gram(const float *y, int64_t rows, int32_t rank, double *g_out, skrp_stream_t stream)
@@ -773,21 +758,6 @@ int skrp_model_inner(const uint32_t *const *coords, const float *values, int64_t
     }
     model_inner_kernel<<<grid_cap((nnz + 7) / 8, 8), 256, 0, s>>>(a, values, nnz, nmodes, lambdas, rank, out);
     SKRP_LAUNCHED("model_inner_kernel");
-    return SKRP_OK;
-}
-
-int skrp_split_columns(const float *src, int64_t rows, int32_t rank, int32_t parts, float *dst,
-                       skrp_stream_t stream)
-{
-    SKRP_REQUIRE(rows >= 0 && parts >= 1 && rank >= 1 && rank % parts == 0 && (rank / parts) % 4 == 0,
-                 "skrp_split_columns: rank %d must split into %d planes of a multiple of 4 columns", rank, parts);
-    if (rows == 0) return SKRP_OK;
-    SKRP_REQUIRE(src && dst && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0,
-                 "skrp_split_columns: null or misaligned pointer");
-    const int R4 = rank / 4;
-    split_columns_kernel<<<grid_for(rows * R4, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const float4 *)src, rows, R4, R4 / parts, (float4 *)dst);
-    SKRP_LAUNCHED("split_columns_kernel");
     return SKRP_OK;
 }
 

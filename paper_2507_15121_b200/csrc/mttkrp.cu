@@ -345,11 +345,11 @@ static Variant mk()
     return v;
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0, int TRED = 0>
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int TRED = 0>
 static Variant mk2()
 {
     Variant v;
-    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, OUTPOL, PF, TRED>;
+    v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, TRED>;
     v.smem = v2_smem_bytes<8 * LPN>();
     return v;
 }
@@ -362,8 +362,8 @@ static bool pick_v2(int R, Variant &v)
     case 16: v = mk2<NM, 2, (NM == 3 ? 2 : 1), 3>(); return true;
     // transpose-reduce row ends (TRED) where VEC >= slots: 7 shuffles + 7 adds
     // per row end instead of 24 + 24 (R=32), 1-2 % per mode on cfg2
-    case 32: v = (NM == 3) ? mk2<NM, 4, 4, 2, 0, 1, 0, 1>() : mk2<NM, 4, 2, 3, 0, 1, 0, 1>(); return true;
-    case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2, 0, 1, 0, 1>(); return true;
+    case 32: v = (NM == 3) ? mk2<NM, 4, 4, 2, 0, 1>() : mk2<NM, 4, 2, 3, 0, 1>(); return true;
+    case 64: v = mk2<NM, 8, (NM == 3 ? 4 : 2), 2, 0, 1>(); return true;
     case 128: v = mk2<NM, 16, (NM == 3 ? 2 : 1), 2>(); return true;
     default: return false;
     }
@@ -384,17 +384,6 @@ static bool pick_fast(int R, Variant &v)
     }
 }
 
-// LDG.128 alternative for R = 32 / 64 (variant 2), kept for A/B tuning.
-template <int NM>
-static bool pick_vec4(int R, Variant &v)
-{
-    switch (R) {
-    case 32: v = mk<NM, 4, 8, 1, 8>(); return true;
-    case 64: v = mk<NM, 4, 16, 1, 4>(); return true;
-    default: return false;
-    }
-}
-
 // Generic: scalar columns, any R <= 256, any N <= SKRP_MAX_MODES.
 static Variant pick_generic(int R)
 {
@@ -411,8 +400,8 @@ static Variant pick_generic(int R)
 
 static bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-// variant: 0 auto (production kernel where it applies), 1 generic scalar,
-// 2 legacy LDG.128, 6 legacy LDG.256
+// variant: 0 = the production kernel where it applies, 1 = the generic
+// scalar tile kernel (a second, independent code path the tests cross-check)
 static Variant choose(const skrp_mttkrp_args &a)
 {
     Variant v{};
@@ -420,87 +409,18 @@ static Variant choose(const skrp_mttkrp_args &a)
     for (int w = 0; w < a.nmodes; ++w) al32 = al32 && (w == a.mode || aligned(a.factors[w], 32));
     if (a.accumulation == SKRP_ACC_DETERMINISTIC) al32 = al32 && aligned(a.carry_vals, 32);
     if (al32 && a.variant != 1) {
-        if (a.variant == 7 && a.rank == 32) {  // occupancy A/B for the production kernel
-            if (a.nmodes == 3) return mk2<3, 4, 2, 2>();
-            if (a.nmodes == 4) return mk2<4, 4, 2, 2>();
-        }
-        if (a.variant == 8 && a.rank == 32) {  // previous default: U=2, 24 warps/SM
-            if (a.nmodes == 3) return mk2<3, 4, 2, 3>();
-            if (a.nmodes == 4) return mk2<4, 4, 4, 2>();
-        }
-        if (a.variant == 10 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1>();  // no L2 hint
-        if (a.variant == 11 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 0>();  // output: no hint
-        if (a.variant == 12 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 1, 0>();  // no factor/output hints
-        if (a.variant == 13 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 0>();  // 24 warps/SM, output normal
-        // streamed-input load policy (pin-one-stream-one shapes): input 0 / 1
-        // loaded without the evict_last hint (19/20) or with evict_first (21/22)
-        if (a.variant == 19 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 2>();
-        if (a.variant == 20 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 4>();
-        if (a.variant == 21 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 10>();
-        if ((a.variant == 27 || a.variant == 28) && a.rank == 32 && a.nmodes == 3) {
-            // A/B: streamed input evict_normal for a hashed 1/2 (27) or 1/4 (28) of its lines
+        if (a.nmodes == 3 && a.rank == 32) {
+            // the streamed input of a pin-one-stream-one layout gathers with
+            // evict_first; class-1 batches use predicated FFMAs (PLAIN bit 64);
+            // row ends transpose-reduce (TRED)
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (a.variant == 27 && sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 202, 1, 0, 1>();
-            if (a.variant == 27 && sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 204, 1, 0, 1>();
-            if (a.variant == 28 && sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 330, 1, 0, 1>();
-            if (a.variant == 28 && sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 332, 1, 0, 1>();
+            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 64 | 2, 1>();
+            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 64 | 4, 1>();
+            return mk2<3, 4, 4, 2, 64, 1>();
         }
-        if (a.variant == 26 && a.rank == 32 && a.nmodes == 3) {  // + predicated class-1 FFMAs
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 74, 1, 0, 1>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 76, 1, 0, 1>();
-            return mk2<3, 4, 4, 2, 64, 1, 0, 1>();
-        }
-        if (a.variant == 25 && a.rank == 32 && a.nmodes == 3) {  // transpose-reduce row ends
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 10, 1, 0, 1>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 12, 1, 0, 1>();
-            return mk2<3, 4, 4, 2, 0, 1, 0, 1>();
-        }
-        if (a.variant == 24 && a.rank == 32 && a.nmodes == 3) {  // + no L1 allocation for the gathers
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 26>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 28>();
-        }
-        if (a.variant == 23 && a.rank == 32 && a.nmodes == 3) {  // 24 warps/SM with the streamed-input policy
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 2, 3, 10>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 2, 3, 12>();
-        }
-        if (a.variant == 22 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 12>();
-        // L2 prefetch of the next batch's rows (A/B)
-        if (a.variant == 17 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 4, 2, 0, 1, 1>();
-        if (a.variant == 18 && a.rank == 32 && a.nmodes == 3) return mk2<3, 4, 2, 3, 0, 1, 1>();
-        // column-pass (R = 16 per pass) A/B variants
-        if (a.variant == 14 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 2>();
-        if (a.variant == 15 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 2, 3, 0, 0>();
-        if (a.variant == 16 && a.rank == 16 && a.nmodes == 3) return mk2<3, 2, 1, 4>();
-        if (a.variant == 9 && a.rank == 64) {
-            if (a.nmodes == 3) return mk2<3, 8, 4, 1>();
-            if (a.nmodes == 4) return mk2<4, 8, 4, 1>();
-        }
-        if (a.variant == 0 && a.nmodes == 3 && a.rank == 32 && a.rle_runs) {  // run-length row ids
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 42, 1, 0, 1>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 44, 1, 0, 1>();
-            return mk2<3, 4, 4, 2, 32, 1, 0, 1>();
-        }
-        if (a.variant == 0 && a.nmodes == 3 && a.rank == 32) {
-            // predicated class-1 FFMAs (PLAIN bit 64): cfg2 133.9 -> 132.2 ms/step
-            const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-            if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 74, 1, 0, 1>();
-            if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 76, 1, 0, 1>();
-            return mk2<3, 4, 4, 2, 64, 1, 0, 1>();
-        }
-        if (a.variant == 0) {
-            if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;
-            if (a.nmodes == 4 && pick_v2<4>(a.rank, v)) return v;
-            if (a.nmodes == 5 && pick_v2<5>(a.rank, v)) return v;
-        }
-        if (a.variant == 2) {
-            if (a.nmodes == 3 && pick_vec4<3>(a.rank, v)) return v;
-            if (a.nmodes == 4 && pick_vec4<4>(a.rank, v)) return v;
-        }
+        if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;
+        if (a.nmodes == 4 && pick_v2<4>(a.rank, v)) return v;
+        if (a.nmodes == 5 && pick_v2<5>(a.rank, v)) return v;
         if (a.nmodes == 3 && pick_fast<3>(a.rank, v)) return v;
         if (a.nmodes == 4 && pick_fast<4>(a.rank, v)) return v;
         if (pick_fast<0>(a.rank, v)) return v;
@@ -518,36 +438,19 @@ struct PanelVariant {
     size_t stage = 0;
 };
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0, int NOTRED = 0>
+template <int NM, int LPN, int U, int NW, int SM = 0>
 static PanelVariant mkp()
 {
-    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, L1NA, ALG, PF, SM, NOTRED>, NW, 8 * LPN,
-                        panel_stage_bytes<8 * LPN, NW, ALG>()};
+    return PanelVariant{mttkrp_panel_kernel<NM, LPN, U, NW, SM>, NW, 8 * LPN, panel_stage_bytes<8 * LPN, NW>()};
 }
 
-static PanelVariant choose_panel(int nmodes, int rank, int variant = 0, int flags = 0)
+static PanelVariant choose_panel(int nmodes, int rank, int flags = 0)
 {
-    if (nmodes == 3 && rank == 32 && variant == 9) {  // A/B: full-butterfly row ends
+    if (nmodes == 3 && rank == 32) {  // streamed input: evict_first loads
         const int sm = flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-        if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 0, 0, 0, 1, 1>();
-        if (sm == SKRP_FLAG_STREAM_INPUT1) return mkp<3, 4, 4, 16, 0, 0, 0, 2, 1>();
+        if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 1>();
+        if (sm == SKRP_FLAG_STREAM_INPUT1) return mkp<3, 4, 4, 16, 2>();
     }
-    if (nmodes == 3 && rank == 32 && variant == 0) {  // streamed input: evict_first loads
-        const int sm = flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
-        if (sm == SKRP_FLAG_STREAM_INPUT0) return mkp<3, 4, 4, 16, 0, 0, 0, 1>();
-        if (sm == SKRP_FLAG_STREAM_INPUT1) return mkp<3, 4, 4, 16, 0, 0, 0, 2>();
-    }
-    // A/B variants (R = 32, N = 3): 1 = gathers without L1 allocation,
-    // 2 = 8 warps per CTA, 3 = both
-    if (nmodes == 3 && rank == 32 && variant == 1) return mkp<3, 4, 4, 16, 1>();
-    if (nmodes == 3 && rank == 32 && variant == 2) return mkp<3, 4, 4, 8>();
-    if (nmodes == 3 && rank == 32 && variant == 3) return mkp<3, 4, 4, 8, 1>();
-    // slot-sequential ranges (ALG 1)
-    if (nmodes == 3 && rank == 32 && variant == 4) return mkp<3, 4, 4, 16, 0, 1>();
-    if (nmodes == 3 && rank == 32 && variant == 5) return mkp<3, 4, 2, 16, 0, 1>();
-    if (nmodes == 3 && rank == 32 && variant == 6) return mkp<3, 4, 8, 16, 0, 1>();
-    if (nmodes == 3 && rank == 32 && variant == 7) return mkp<3, 4, 4, 16, 0, 0, 1>();  // L2 prefetch
-    if (nmodes == 3 && rank == 32 && variant == 8) return mkp<3, 4, 4, 16, 0, 2>();  // one-step staging
     if (nmodes == 3) {
         switch (rank) {
         case 8: return mkp<3, 1, 1, 16>();
@@ -628,24 +531,7 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
     ctas = std::min<int64_t>(ctas, (a.num_tiles + kWarpsPerCta - 1) / kWarpsPerCta);
     SKRP_CUDA(cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), s));
     unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
-    if (v.v2 && a.l2_window_bytes > 0) {
-        // pinned factor block: persisting hits in the set-aside L2, streaming misses
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kWarpsPerCta * 32);
-        cfg.dynamicSmemBytes = v.smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(a.l2_window_base);
-        attr[0].val.accessPolicyWindow.num_bytes = (size_t)a.l2_window_bytes;
-        attr[0].val.accessPolicyWindow.hitRatio = a.l2_window_hit_ratio;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        SKRP_CUDA(cudaLaunchKernelEx(&cfg, v.v2, a, (a.flags & SKRP_FLAG_ADDITIVE) ? 1 : 0));
-    } else if (v.v2) {
+    if (v.v2) {
         v.v2<<<grid, kWarpsPerCta * 32, v.smem, s>>>(a, (a.flags & SKRP_FLAG_ADDITIVE) ? 1 : 0);
     } else {
         v.fn<<<grid, kWarpsPerCta * 32, 0, s>>>(a);
@@ -657,7 +543,7 @@ int skrp_mttkrp_tiles(const skrp_mttkrp_args *args, skrp_stream_t stream)
 
 int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows)
 {
-    PanelVariant v = choose_panel(nmodes, rank, 0);
+    PanelVariant v = choose_panel(nmodes, rank);
     SKRP_REQUIRE(v.fn != nullptr, "no panel kernel for nmodes=%d rank=%d (ranks 8/16/32/64, 3..5 modes)", nmodes,
                  rank);
     if (warps) *warps = v.warps;
@@ -674,7 +560,7 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
     SKRP_REQUIRE(a.mode >= 0 && a.mode < a.nmodes, "mode %d out of range", a.mode);
     SKRP_REQUIRE(p.num_items >= 0 && p.groups >= 1, "bad item count / groups");
     if (p.num_items == 0) return SKRP_OK;
-    PanelVariant v = choose_panel(a.nmodes, a.rank, a.variant, a.flags);
+    PanelVariant v = choose_panel(a.nmodes, a.rank, a.flags);
     SKRP_REQUIRE(v.fn != nullptr, "no panel kernel for nmodes=%d rank=%d", a.nmodes, a.rank);
     SKRP_REQUIRE(p.warps == v.warps, "panel layout built for %d warps, kernel uses %d", p.warps, v.warps);
     SKRP_REQUIRE(p.slab_rows >= p.warps && (p.slab_rows & (p.slab_rows - 1)) == 0 && p.slab_rows <= panel_max_slab(v),

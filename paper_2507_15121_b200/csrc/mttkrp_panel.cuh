@@ -47,7 +47,8 @@ __device__ __forceinline__ void grid_wait(unsigned long long *counter, unsigned 
     }
 }
 
-template <int NM, int LPN, int U, int NW, int L1NA = 0, int ALG = 0, int PF = 0, int SM = 0, int NOTRED = 0>
+// SM bit j: input j is the streamed input (evict_first gathers)
+template <int NM, int LPN, int U, int NW, int SM = 0>
 __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     mttkrp_panel_kernel(const skrp_mttkrp_args a, const skrp_panel_args pa)
 {
@@ -58,15 +59,12 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     constexpr int STR = RR + 4;
     constexpr int NIN = NM - 1;
     constexpr int CPL = (RR + 31) / 32;
-    static_assert(ALG == 1 || 32 % G == 0, "groups must tile the 32-nonzero batch");
+    static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     extern __shared__ __align__(16) float smem_p[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int slab_rows = pa.slab_rows;
-    // ALG 2 stages only one step of S nonzeros (the S slots) for class-2
-    // batches, so the staging area shrinks 3.7x and the SM keeps its L1 for
-    // the gathers in flight
-    constexpr int SROWS = ALG == 2 ? S : 32;
+    constexpr int SROWS = 32;
     float *panel = smem_p;                                          // slab_rows x RR
     float *stage = panel + (size_t)slab_rows * RR + (size_t)wib * ((SROWS + 1) * STR);
     float *carry_row = stage + SROWS * STR;
@@ -105,7 +103,6 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
         reinterpret_cast<float4 *>(panel)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     const bool lockstep = (pa.flags & SKRP_PANEL_LOCKSTEP) != 0;
-    const bool group_sync = (pa.flags & SKRP_PANEL_GROUP_SYNC) != 0;
     for (int64_t round = 0;; ++round) {
         __syncthreads();  // previous item's write-back / zeroing done
         int64_t item;
@@ -135,147 +132,9 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
         // panel row of an output row, and the read-add-write flushes
         auto prow = [&](uint32_t row) { return panel + (size_t)(row - slab_base) * RR; };
 
-        // ALG 1 (slot-sequential): slot s of the warp walks its own contiguous
-        // chunk of the range (len*s/S .. len*(s+1)/S), one nonzero per slot
-        // per step (U steps unrolled), keeping the current row's run in
-        // registers.  Runs that start and end inside the chunk are flushed
-        // with a plain read-add-write (no other slot holds that row); the
-        // chunk's first and last runs (possibly shared with the neighbouring
-        // chunks) are staged and merged column-parallel in row order at the
-        // end of the range.  No per-batch ballots / row classes.
-        auto slot_range = [&](int64_t b0, int64_t b1) {
-            constexpr int PER = (U + LPN - 1) / LPN;
-            constexpr uint32_t NONE = 0xffffffffu;
-            static_assert(ALG == 0 || 2 * S * RR + 2 * S <= 33 * STR, "slot staging does not fit");
-            const int64_t len = b1 - b0;
-            const int64_t e0 = b0 + (len * slot) / S, e1 = b0 + (len * (slot + 1)) / S;
-            const int64_t steps = ((len + S - 1) / S + U - 1) / U;
-            uint32_t m_r[PER], m_c[PER][NIN];
-            float m_v[PER];
-            auto fetch = [&](int64_t sb) {
-#pragma unroll
-                for (int q = 0; q < PER; ++q) {
-                    const int64_t e = sb + sl + q * LPN;
-                    const bool ok = e < e1;
-                    const int64_t idx = ok ? e : (e1 > e0 ? e1 - 1 : b0);
-                    const uint32_t r = ld_stream_u32(rowc + idx, pol_stream);
-                    m_r[q] = ok ? r : NONE;
-                    m_v[q] = ok ? ld_stream_f32(a.values + idx, pol_stream) : 0.f;
-#pragma unroll
-                    for (int j = 0; j < NIN; ++j) m_c[q][j] = ld_stream_u32(C[j] + idx, pol_stream);
-                }
-            };
-            uint32_t cur = NONE, rowF = NONE;
-            bool have_first = false;
-            float acc[VEC], accF[VEC];
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) acc[i] = accF[i] = 0.f;
-            fetch(e0);
-            for (int64_t st = 0; st < steps; ++st) {
-                uint32_t l_r[PER], l_c[PER][NIN];
-                float l_v[PER];
-#pragma unroll
-                for (int q = 0; q < PER; ++q) {
-                    l_r[q] = m_r[q];
-                    l_v[q] = m_v[q];
-#pragma unroll
-                    for (int j = 0; j < NIN; ++j) l_c[q][j] = m_c[q][j];
-                }
-                if (st + 1 < steps) fetch(e0 + (st + 1) * U);
-                float gv[U][NIN][VEC];
-                float vv[U];
-                uint32_t rr[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int src = slot * LPN + (u % LPN);
-                    rr[u] = __shfl_sync(kFull, l_r[u / LPN], src);
-                    vv[u] = __shfl_sync(kFull, l_v[u / LPN], src);
-#pragma unroll
-                    for (int j = 0; j < NIN; ++j) {
-                        const uint32_t idx = __shfl_sync(kFull, l_c[u / LPN][j], src);
-                        if constexpr (L1NA) ld_row8_na(gv[u][j], frow(j, idx), pol_row);
-                        else ld_row<VEC>(gv[u][j], frow(j, idx), 0);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (rr[u] != NONE && rr[u] != cur) {
-                        if (cur != NONE) {
-                            if (!have_first) {
-#pragma unroll
-                                for (int i = 0; i < VEC; ++i) accF[i] = acc[i];
-                                rowF = cur;
-                                have_first = true;
-                            } else {
-                                rmw_add_vec<VEC>(prow(cur) + col, acc);
-                            }
-                        }
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-                        cur = rr[u];
-                    }
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) {
-                        float p = vv[u];
-#pragma unroll
-                        for (int j = 0; j < NIN - 1; ++j) p *= gv[u][j][i];
-                        acc[i] = fmaf(p, gv[u][NIN - 1][i], acc[i]);
-                    }
-                }
-            }
-            // chunk-boundary runs: stage (first, last) per slot, merge in order
-            uint32_t *erow = reinterpret_cast<uint32_t *>(stage + 2 * S * RR);
-            store_vec<VEC>(stage + (2 * slot) * RR + col, accF);
-            store_vec<VEC>(stage + (2 * slot + 1) * RR + col, acc);
-            if (sl == 0) {
-                erow[2 * slot] = rowF;
-                erow[2 * slot + 1] = cur;
-            }
-            __syncwarp();
-            float run[CPL];
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) run[q] = 0.f;
-            uint32_t rrow = NONE;
-            for (int k = 0; k < 2 * S; ++k) {
-                const uint32_t r = erow[k];
-                if (r == NONE) continue;
-                if (r != rrow) {
-                    if (rrow != NONE) {
-                        float *pr = prow(rrow);
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) {
-                            const int c = lane + 32 * q;
-                            if (c < RR) pr[c] += run[q];
-                            run[q] = 0.f;
-                        }
-                    }
-                    rrow = r;
-                }
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) {
-                    const int c = lane + 32 * q;
-                    if (c < RR) run[q] += stage[k * RR + c];
-                }
-            }
-            if (rrow != NONE) {
-                float *pr = prow(rrow);
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) {
-                    const int c = lane + 32 * q;
-                    if (c < RR) pr[c] += run[q];
-                }
-            }
-            __syncwarp();
-        };
-
         for (int g = 0; g < pa.groups; ++g) {
-            if (group_sync && g > 0) __syncthreads();  // uniform trip count: every warp arrives
             const int64_t b0 = offs[g * NW + wib], b1 = offs[g * NW + wib + 1];
             if (b0 >= b1) continue;
-            if constexpr (ALG == 1) {
-                slot_range(b0, b1);
-                continue;
-            }
             float acc[VEC];
 #pragma unroll
             for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
@@ -289,7 +148,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             // column sums and add them to the panel row themselves
             constexpr int NV = (VEC >= S) ? VEC / S : 1;
             auto reduce_write = [&](uint32_t row) {
-                if constexpr (VEC >= S && !NOTRED) {
+                if constexpr (VEC >= S) {
                     float w[VEC];
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) w[i] = acc[i];
@@ -318,10 +177,6 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             };
             uint32_t nr_l, nc_l[NIN];
             float nv_l;
-            // PF: metadata two batches ahead; the rows of batch i+1 are prefetched
-            // into L2 while batch i gathers (no registers held by the prefetches)
-            uint32_t fr_l = 0, fc_l[NIN];
-            float fv_l = 0.f;
             auto fetch_to = [&](int64_t nbase, uint32_t &r, float &vv_, uint32_t (&c)[NIN]) {
                 const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
                 const bool v = lane < nn;
@@ -334,27 +189,9 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
             auto fetch = [&](int64_t nbase) { fetch_to(nbase, nr_l, nv_l, nc_l); };
             // advance the metadata pipeline at the start of the batch at `base`
             auto advance = [&](int64_t base) {
-                if constexpr (PF) {
-                    if (base + 32 < b1) {
-                        nr_l = fr_l;
-                        nv_l = fv_l;
-#pragma unroll
-                        for (int j = 0; j < NIN; ++j) {
-                            nc_l[j] = fc_l[j];
-                            const float *rowp = F[j] + (size_t)fc_l[j] * fld;
-#pragma unroll
-                            for (int k = 0; k < (RR * 4 + 127) / 128; ++k) prefetch_l2_last(rowp + 32 * k);
-                        }
-                        if (base + 64 < b1) fetch_to(base + 64, fr_l, fv_l, fc_l);
-                    }
-                } else {
-                    if (base + 32 < b1) fetch(base + 32);
-                }
+                if (base + 32 < b1) fetch(base + 32);
             };
             fetch(b0);
-            if constexpr (PF) {
-                if (b0 + 32 < b1) fetch_to(b0 + 32, fr_l, fv_l, fc_l);
-            }
             uint32_t cur = __shfl_sync(kFull, nr_l, 0);
             for (int64_t base = b0; base < b1; base += 32) {
                 const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
@@ -390,31 +227,17 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                         if (slot == 0) store_vec<VEC>(carry_row + col, acc);
                     }
                 }
-                // ALG 2 class-2 state: the open row and its column-layout run
-                float c2run[CPL];
-                uint32_t c2row = cur;
-                if constexpr (ALG == 2) {
-                    if (cls == 2) {
-                        __syncwarp();
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) {
-                            const int c = lane + 32 * q;
-                            c2run[q] = (c < RR) ? carry_row[c] : 0.f;
-                        }
-                    }
-                }
                 auto group = [&](int g0) {
                     float gv[U][NIN][VEC];
                     float vv[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int e = g0 + (ALG == 2 ? u * S + slot : slot * U + u);
+                        const int e = g0 + slot * U + u;
                         vv[u] = __shfl_sync(kFull, v_l, e);
 #pragma unroll
                         for (int j = 0; j < NIN; ++j) {
                             const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                            if constexpr (L1NA) ld_row8_na(gv[u][j], frow(j, idx), pol_row);
-                            else if ((SM >> j) & 1) ld_row8_first(gv[u][j], frow(j, idx));
+                            if ((SM >> j) & 1) ld_row8_first(gv[u][j], frow(j, idx));
                             else ld_row<VEC>(gv[u][j], frow(j, idx), 0);
                         }
                     }
@@ -431,7 +254,7 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                     } else if (cls == 1) {
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
-                            const bool inA = g0 + (ALG == 2 ? u * S + slot : slot * U + u) < e_b;
+                            const bool inA = g0 + slot * U + u < e_b;
                             float p[VEC];
 #pragma unroll
                             for (int i = 0; i < VEC; ++i) {
@@ -442,41 +265,6 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                             // predicated FFMAs, no FSEL per float (as in mttkrp_v2)
 #pragma unroll
                             for (int i = 0; i < VEC; i += 4) fma4_split(inA, p + i, gv[u][NIN - 1] + i, acc + i, accB + i);
-                        }
-                    } else if constexpr (ALG == 2) {
-                        // one step (S consecutive nonzeros) at a time: stage,
-                        // then fold the S rows in order into the open run
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            float p[VEC];
-#pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                p[i] = vv[u];
-#pragma unroll
-                                for (int j = 0; j < NIN; ++j) p[i] *= gv[u][j][i];
-                            }
-                            store_vec<VEC>(stage + slot * STR + col, p);
-                            __syncwarp();
-                            const int e0 = g0 + u * S;
-                            for (int k = 0; k < S && e0 + k < nin; ++k) {
-                                const int e = e0 + k;
-                                if ((cm >> e) & 1u) {
-                                    float *pr = prow(c2row);
-#pragma unroll
-                                    for (int q = 0; q < CPL; ++q) {
-                                        const int c = lane + 32 * q;
-                                        if (c < RR) pr[c] += c2run[q];
-                                        c2run[q] = 0.f;
-                                    }
-                                    c2row = __shfl_sync(kFull, r_l, e);
-                                }
-#pragma unroll
-                                for (int q = 0; q < CPL; ++q) {
-                                    const int c = lane + 32 * q;
-                                    if (c < RR) c2run[q] += stage[k * STR + c];
-                                }
-                            }
-                            __syncwarp();
                         }
                     } else {
 #pragma unroll
@@ -501,19 +289,6 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                     cur = __shfl_sync(kFull, r_l, e_b);
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) acc[i] = accB[i];
-                    continue;
-                }
-                if constexpr (ALG == 2) {
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        const int c = lane + 32 * q;
-                        if (c < RR) carry_row[c] = c2run[q];
-                    }
-                    __syncwarp();
-                    cur = c2row;
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
-                    __syncwarp();
                     continue;
                 }
                 // class 2: segmented column sums over the staged rows
@@ -608,8 +383,8 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
     }
 }
 
-template <int RR, int NW, int ALG = 0>
+template <int RR, int NW>
 constexpr size_t panel_stage_bytes()
 {
-    return sizeof(float) * NW * (((ALG == 2 ? 32 / (RR / 8) : 32) + 1) * (RR + 4));
+    return sizeof(float) * NW * (33 * (RR + 4));
 }

@@ -49,7 +49,11 @@ __device__ __forceinline__ void out_rmw(float *p, const float (&v)[VEC], uint64_
     }
 }
 
-template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int OUTPOL = 1, int PF = 0, int TRED = 0>
+// PLAIN bit 1 / 2: input 0 / 1 is the STREAMED input of a pin-one-stream-one
+// layout (evict_first gathers, so it does not displace the pinned block);
+// bit 64: class-1 batches accumulate with predicated FFMAs.  TRED: row ends
+// transpose-reduce across the slots.
+template <int NM, int LPN, int U, int MINB, int PLAIN = 0, int TRED = 0>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     mttkrp_v2_kernel(const skrp_mttkrp_args a, int additive)
 {
@@ -62,12 +66,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     auto srow_skew = [](int e) { return (LPN == 4 && ((e / U) & 1)) ? 4 : 0; };
     constexpr int NIN = NM - 1;     // input modes per nonzero
     constexpr int CPL = (RR + 31) / 32;  // columns per lane in the column layout
-    // PLAIN bits 0..4 pick the gather cache policies (below); bit 5 (32) reads
-    // the output-row ids run-length encoded (a.rle_*): change bits + per-word
-    // run prefix + one id per run instead of one u32 per nonzero
-    constexpr int PL = PLAIN & 31;
-    constexpr bool RLE = (PLAIN & 32) != 0;
-    // bit 6 (64): class-1 batches accumulate with predicated FFMAs
+    constexpr int STREAMED = PLAIN & 6;
     constexpr bool SPLITFMA = (PLAIN & 64) != 0;
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     extern __shared__ __align__(16) float smem_v2[];
@@ -88,19 +87,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     const size_t old = a.out_ld > 0 ? (size_t)a.out_ld : (size_t)RR;
     const uint32_t *__restrict__ rowc = a.coords[mode];
     const uint64_t pol_stream = policy_evict_first();
-    // PLAIN bits 7/8 (128/256): the streamed input's rows get evict_normal
-    // for a hashed 1/2 (1/4) of its lines, evict_first for the rest
-    uint64_t pol_sfrac = 0;
-    if constexpr ((PLAIN & 384) == 128)
-        asm("createpolicy.fractional.L2::evict_normal.L2::evict_first.b64 %0, 0.5;" : "=l"(pol_sfrac));
-    else if constexpr ((PLAIN & 384) == 256)
-        asm("createpolicy.fractional.L2::evict_normal.L2::evict_first.b64 %0, 0.25;" : "=l"(pol_sfrac));
     const uint64_t pol_row = policy_evict_last();
-    // output rows: evict_first (OUTPOL) so the per-group sweep of output lines
-    // does not evict the group's factor blocks; else the default policy
-    uint64_t pol_out;
-    if constexpr (OUTPOL) pol_out = policy_evict_first();
-    else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_out));
+    // output rows: evict_first so the per-group sweep of output lines does not
+    // evict the group's factor blocks
+    const uint64_t pol_out = policy_evict_first();
     const bool det = a.accumulation == SKRP_ACC_DETERMINISTIC;
     // input modes in ascending order (kernels.py:63-69): j-th input = j or j+1
     const float *__restrict__ F[NIN];
@@ -118,16 +108,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         return reinterpret_cast<const float *>(Fcol[j] + (uint64_t)idx * fld_bytes);
     };
 
-    // row id of nonzero p: the run it lies in is (#change bits at <= p) - 1
-    auto row_at = [&](int64_t p) -> uint32_t {
-        if constexpr (RLE) {
-            const int64_t w = p >> 5;
-            const uint32_t m = __ldg(a.rle_chg + w) & (0xffffffffu >> (31 - (int)(p & 31)));
-            return __ldg(a.rle_runs + __ldg(a.rle_pre + w) + __popc(m) - 1);
-        } else {
-            return rowc[p];
-        }
-    };
 
     for (;;) {
         unsigned long long claimed = 0;
@@ -135,13 +115,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         const int64_t t = (int64_t)__shfl_sync(kFull, claimed, 0);
         if (t >= a.num_tiles) break;
         const int64_t b0 = a.tiles[2 * t], b1 = a.tiles[2 * t + 1];
-        const int64_t prev_row = b0 > 0 ? (int64_t)row_at(b0 - 1) : -1;
-        const int64_t next_row = b1 < a.nnz ? (int64_t)row_at(b1) : -1;
+        const int64_t prev_row = b0 > 0 ? (int64_t)rowc[b0 - 1] : -1;
+        const int64_t next_row = b1 < a.nnz ? (int64_t)rowc[b1] : -1;
         if (det && lane == 0) {
             a.carry_rows[2 * t] = -1;
             a.carry_rows[2 * t + 1] = -1;
         }
-        uint32_t cur = row_at(b0);
+        uint32_t cur = rowc[b0];
         bool head = true;
         float acc[VEC];
 #pragma unroll
@@ -238,26 +218,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         // the gather addresses never wait on a fresh metadata miss
         uint32_t nr_l, nc_l[NIN];
         float nv_l;
-        // PF: metadata two batches ahead; the rows of batch i+1 are prefetched
-        // into L2 while batch i gathers (no registers held by the prefetches)
-        uint32_t fr_l = 0, fc_l[NIN];
-        float fv_l = 0.f;
         auto fetch_to = [&](int64_t nbase, uint32_t &r, float &vv_, uint32_t (&c)[NIN]) {
             const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
             const bool v = lane < nn;
             const int64_t src = nbase + (v ? lane : nn - 1);
-            if constexpr (RLE) {
-                // the batch's 32 change bits straddle two words (uniform loads)
-                const int64_t w = nbase >> 5;
-                const int sh = (int)(nbase & 31);
-                const uint32_t m0 = __ldg(a.rle_chg + w), m1 = __ldg(a.rle_chg + w + 1);
-                const uint32_t win = __funnelshift_r(m0, m1, sh);
-                const uint32_t before = __ldg(a.rle_pre + w) + __popc(m0 & ((1u << sh) - 1u));
-                const int li = v ? lane : nn - 1;
-                r = __ldg(a.rle_runs + before + __popc(win & (0xffffffffu >> (31 - li))) - 1);
-            } else {
-                r = ld_stream_u32(rowc + src, pol_stream);
-            }
+            r = ld_stream_u32(rowc + src, pol_stream);
             vv_ = v ? ld_stream_f32(a.values + src, pol_stream) : 0.f;
 #pragma unroll
             for (int j = 0; j < NIN; ++j) c[j] = ld_stream_u32(C[j] + src, pol_stream);
@@ -265,27 +230,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         auto fetch = [&](int64_t nbase) { fetch_to(nbase, nr_l, nv_l, nc_l); };
         // advance the metadata pipeline at the start of the batch at `base`
         auto advance = [&](int64_t base) {
-            if constexpr (PF) {
-                if (base + 32 < b1) {
-                    nr_l = fr_l;
-                    nv_l = fv_l;
-#pragma unroll
-                    for (int j = 0; j < NIN; ++j) {
-                        nc_l[j] = fc_l[j];
-                        const float *rowp = F[j] + (size_t)fc_l[j] * fld;
-#pragma unroll
-                        for (int k = 0; k < (RR * 4 + 127) / 128; ++k) prefetch_l2_last(rowp + 32 * k);
-                    }
-                    if (base + 64 < b1) fetch_to(base + 64, fr_l, fv_l, fc_l);
-                }
-            } else {
-                if (base + 32 < b1) fetch(base + 32);
-            }
+            if (base + 32 < b1) fetch(base + 32);
         };
         fetch(b0);
-        if constexpr (PF) {
-            if (b0 + 32 < b1) fetch_to(b0 + 32, fr_l, fv_l, fc_l);
-        }
         for (int64_t base = b0; base < b1; base += 32) {
             // a short last batch is padded with copies of its last nonzero
             // carrying value 0: same row (no extra boundary), valid
@@ -352,23 +299,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < NIN; ++j) {
                         const uint32_t idx = __shfl_sync(kFull, c_l[j], e);
-                        // PLAIN: 1 = no L2 hint on every input; bits 1/2 (+4) mark
-                        // input 0/1 as streamed (evict_first 4-bit variants) so it
-                        // does not displace the pinned block of the other input
-                        if constexpr (PL == 1) ld_row8_plain(g[u][j], frow(j, idx));
-                        else if constexpr (PL >= 2) {
-                            // bit 4 (16): no L1 allocation for any gather
-                            if ((PL >> (j + 1)) & 1) {
-                                if constexpr (PLAIN & 384) ld_row8_hint(g[u][j], frow(j, idx), pol_sfrac);
-                                else if constexpr ((PL & 8) && (PL & 16))
-                                    ld_row8_first_na(g[u][j], frow(j, idx));
-                                else if constexpr (PL & 8) ld_row8_first(g[u][j], frow(j, idx));
-                                else ld_row8_plain(g[u][j], frow(j, idx));
-                            } else {
-                                if constexpr (PL & 16) ld_row8_last_na(g[u][j], frow(j, idx));
-                                else ld_row<VEC>(g[u][j], frow(j, idx), pol_row);
-                            }
-                        }
+                        if ((STREAMED >> (j + 1)) & 1) ld_row8_first(g[u][j], frow(j, idx));
                         else ld_row<VEC>(g[u][j], frow(j, idx), pol_row);
                     }
                 }

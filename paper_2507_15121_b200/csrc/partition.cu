@@ -536,65 +536,3 @@ extern "C" int skrp_block_keys(const uint32_t *const *coords, int32_t nmodes, co
     SKRP_LAUNCHED("block_keys_kernel");
     return SKRP_OK;
 }
-
-// ------------------------------------------------- run-length output rows
-// The tile kernel reads one u32 row id per nonzero (nnz x 4 B of the per-mode
-// stream); rows come in runs (cfg2: ~50 nonzeros per row per block group), so
-// a change-bit word per 32 nonzeros + a per-word run prefix + one id per run
-// carry the same information in ~0.35 B per nonzero.
-namespace skrp {
-
-__global__ void rle_mark_kernel(const uint32_t *__restrict__ rows, int64_t n, int64_t words,
-                                uint32_t *__restrict__ chg, int64_t *__restrict__ counts)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words; w += nwarps) {
-        const int64_t i = w * 32 + lane;
-        const bool f = i < n && (i == 0 || rows[i] != rows[i - 1]);
-        const uint32_t m = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) {
-            chg[w] = m;
-            counts[w] = __popc(m);
-        }
-    }
-}
-
-__global__ void rle_runs_kernel(const uint32_t *__restrict__ rows, int64_t n, int64_t words,
-                                const uint32_t *__restrict__ chg, const int64_t *__restrict__ prefix,
-                                uint32_t *__restrict__ pre, uint32_t *__restrict__ runs)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words; w += nwarps) {
-        const uint32_t m = chg[w];
-        const int64_t p = prefix[w];
-        if (lane == 0) pre[w] = (uint32_t)p;
-        if ((m >> lane) & 1u) runs[p + __popc(m & ((1u << lane) - 1u))] = rows[w * 32 + lane];
-    }
-}
-
-}  // namespace skrp
-
-extern "C" int skrp_rle_mark(const uint32_t *rows, int64_t n, uint32_t *chg, int64_t *counts, skrp_stream_t stream)
-{
-    SKRP_REQUIRE(n >= 0 && n < (int64_t(1) << 32), "skrp_rle_mark: n must be in [0, 2^32)");
-    const int64_t words = n / 32 + 1;  // + the zero tail word the kernel's window reads
-    SKRP_REQUIRE(chg && counts && (rows || n == 0), "skrp_rle_mark: null pointer");
-    const int64_t wpad = words + 1;
-    rle_mark_kernel<<<grid_for(wpad * 32, 256), 256, 0, (cudaStream_t)stream>>>(rows, n, wpad, chg, counts);
-    SKRP_LAUNCHED("rle_mark_kernel");
-    return SKRP_OK;
-}
-
-extern "C" int skrp_rle_runs(const uint32_t *rows, int64_t n, const uint32_t *chg, const int64_t *prefix,
-                             uint32_t *pre, uint32_t *runs, skrp_stream_t stream)
-{
-    SKRP_REQUIRE(n >= 0 && n < (int64_t(1) << 32), "skrp_rle_runs: n must be in [0, 2^32)");
-    SKRP_REQUIRE(chg && prefix && pre && (runs || n == 0) && (rows || n == 0), "skrp_rle_runs: null pointer");
-    const int64_t wpad = n / 32 + 2;
-    rle_runs_kernel<<<grid_for(wpad * 32, 256), 256, 0, (cudaStream_t)stream>>>(rows, n, wpad, chg, prefix, pre,
-                                                                                runs);
-    SKRP_LAUNCHED("rle_runs_kernel");
-    return SKRP_OK;
-}

@@ -293,6 +293,7 @@ class DistributedMttkrp:
         ``exchange=False`` skips the all-gather (one rank's compute alone:
         bench.py --emulate-world runs every rank's share on one GPU)."""
         import torch
+        from torch.cuda import nvtx
 
         rank_r = factors[0].shape[1]
         if self.outputs is None or self._rank_r != rank_r or self.outputs[0].dtype != factors[0].dtype:
@@ -300,13 +301,17 @@ class DistributedMttkrp:
         self._exchange = exchange
         facs = list(factors)
         for d, plan in enumerate(self.plans):
+            nvtx.range_push(f"skrp mode {plan.mode} mttkrp")
             out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
                                    out=None if outputs is None else outputs[d])
+            nvtx.range_pop()
             if self.world > 1 and exchange:
+                nvtx.range_push(f"skrp mode {plan.mode} all-gather")
                 if outputs is None and self._fused(d):
                     self._peer_sync()  # rows were pushed by every rank's kernel
                 else:
                     allgather_owned_rows(out, self.ownership[d], self.group, ledger, step=d)
+                nvtx.range_pop()
             if after_mode is not None:
                 after_mode(d, out)
             if chained:

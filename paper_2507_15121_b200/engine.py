@@ -60,24 +60,17 @@ class PlatformConfig:
     scheduling: str = "dynamic"
     # B200 knobs (defaults keep the reference's fields and meaning intact)
     tile_nnz: int = 0           # nonzeros per work-queue tile (a slice of one ISP); 0 = auto
-    kernel_variant: int = 0     # 0 auto, 1 generic scalar, 2 LDG.128 rows (A/B tuning)
+    kernel_variant: int = 0     # 0 = production kernel, 1 = generic scalar tile kernel (cross-check path)
     carry_chunk: int = 256      # carry-tree fan-in
     layout: str = "flycoo"      # "flycoo" (plan order), "blocked" (L2-blocked), "auto" (cost model)
     l2_budget_mb: int = 192     # L2 bytes the blocked layout plans on (B200-calibrated)
     max_blocks: int = 8         # blocks per input mode the layout search may use (B200-tuned)
-    col_passes: int = 1         # column passes: each pass gathers R/col_passes columns per factor row,
-                                # so a pass's L2 working set is 1/col_passes of the rows' bytes (atomic only)
-    col_planes: bool = True     # column passes read contiguous column planes (else strided row slices)
     panel_l2_mb: int = -1       # panel layout: >= 0 cuts input modes to this L2 budget; -1 = blocked cost model
     slab_rows: int = 0          # panel layout: output rows per slab (0 = auto, see panel_smem_kb)
     panel_smem_kb: int = 64     # panel layout: shared memory for the output panel (auto slab size)
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
-    panel_group_sync: bool = False  # panel layout: a CTA barrier before every block group
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
-    l2_window_mb: int = 0       # >0: per-group launches with an L2 access-policy window on the pinned block
-    rle_rows: bool = False      # tile kernel reads run-length output-row ids (R=32, N=3)
-    slot_block_shift: int = 0   # slot layout: input blocks of 2^shift rows (0 = auto, 32 MB blocks)
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -88,12 +81,12 @@ class PlatformConfig:
             raise ValueError(f"accumulation must be one of {ACCUMULATION_MODES}")
         if self.scheduling not in SCHEDULING_MODES:
             raise ValueError(f"scheduling must be one of {SCHEDULING_MODES}")
+        if self.kernel_variant not in (0, 1):
+            raise ValueError("kernel_variant must be 0 (production) or 1 (generic scalar)")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
-        if self.layout not in ("flycoo", "blocked", "panel", "slots", "auto"):
-            raise ValueError("layout must be 'flycoo', 'blocked', 'panel', 'slots' or 'auto'")
-        if self.col_passes < 1 or self.col_passes & (self.col_passes - 1):
-            raise ValueError("col_passes must be a power of two >= 1")
+        if self.layout not in ("flycoo", "blocked", "panel", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked', 'panel' or 'auto'")
 
 
 
@@ -136,20 +129,30 @@ def _as_device_factor(f, dev):
         f = f.data
     if isinstance(f, torch.Tensor):
         return f.to(dev, dtype=torch.float32).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).to(dev, dtype=torch.float32)
+    from .hostio import upload_f64
+
+    return upload_f64(f, dev)
 
 
 def make_devices(factors, cfg: PlatformConfig) -> list:
     """One DeviceState per device, each with its own fp32 factor replicas
-    (engine.py:83-88); device j lives on GPU j mod torch.cuda.device_count()."""
+    (engine.py:83-88); device j lives on GPU j mod torch.cuda.device_count().
+    Host factors cross PCIe once per physical GPU (pinned staging, converted
+    on the GPU, hostio.upload_f64); further replicas on that GPU are device
+    copies."""
     torch = _torch()
     ngpu = torch.cuda.device_count()
     if ngpu == 0:
         raise RuntimeError("make_devices: no CUDA device visible (the B200 engine has no CPU path)")
-    devs = []
+    devs, first = [], {}
     for j in range(cfg.devices):
         gpu = torch.device("cuda", j % ngpu)
-        devs.append(DeviceState(j, [_as_device_factor(f, gpu) for f in factors], cuda_device=gpu))
+        if gpu.index in first:
+            facs = [f.clone() for f in first[gpu.index]]
+        else:
+            facs = [_as_device_factor(f, gpu) for f in factors]
+            first[gpu.index] = facs
+        devs.append(DeviceState(j, facs, cuda_device=gpu))
     return devs
 
 
@@ -353,11 +356,6 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
         return plan
-    if cfg.layout == "slots":
-        if len(plan.shape) != 3 or rank != 32:
-            raise ValueError("slot layout needs N = 3 and R = 32")
-        plan.to_slots(slot_blocking(plan, rank, shift=cfg.slot_block_shift))
-        return plan
     if cfg.layout == "panel":
         prm = choose_panels(plan, rank, cfg, shard_ids)
         if prm is None:
@@ -446,16 +444,7 @@ class _ShardExec:
         self.nnz = (int(clip[1] - clip[0]) if clip is not None
                     else int(sum(plan.shards[j].nnz for j in shard_ids)))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(plan_global_nnz(plan), gpu)
-        # L2 window: one launch per group whose pinned block gets an access-policy
-        # window (persisting set-aside L2); pin-one-stream-one layouts only
-        self.window = None
-        if cfg.l2_window_mb > 0 and self.blocked and not self.det and plan.block_shifts is not None:
-            ins = [w for w in range(len(plan.shape)) if w != plan.mode and plan.block_shifts[w] >= 0]
-            if len(ins) == 1:
-                self.window = (ins[0], plan.block_shifts[ins[0]])
-                got = ctypes.c_int64()
-                _lib.call("skrp_set_l2_persisting", cfg.l2_window_mb << 20, ctypes.byref(got))
-        if self.blocked and (self.det or self.window is not None):
+        if self.blocked and self.det:
             keys = sorted({int(k) for j in shard_ids if plan.shards[j].nnz for k in plan.groups[j][:, 2]})
         else:
             keys = [None]
@@ -475,17 +464,8 @@ class _ShardExec:
                         lvl["vals_out"] = torch.empty(2 * nch * rank, dtype=torch.float64, device=gpu)
                     seg["levels"].append(lvl)
             self.segments.append(seg)
-        # column passes (atomic discipline, production-kernel ranks only)
-        P = cfg.col_passes
-        w = rank // P if rank % P == 0 else 0
-        self.passes = P if (P > 1 and not self.det and w in _V2_RANKS) else 1
-        self.planes_mode = cfg.col_planes
-        self._planes = {}
-        self._nin = len(plan.shape) - 1
+        self.passes = 1
         self.num_tiles = sum(sg["n"] for sg in self.segments)
-        self.rle = None
-        if cfg.rle_rows and rank == 32 and len(plan.shape) == 3 and self.passes == 1 and self.num_tiles:
-            self.rle = _plan_rle(plan, gpu)
         self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
         mx = max((sg["n"] for sg in self.segments), default=0)
         if self.det and mx:
@@ -500,31 +480,7 @@ class _ShardExec:
 
     @property
     def launches(self) -> int:
-        per = sum(1 + len(sg["levels"]) for sg in self.segments)
-        if self.passes == 1:
-            return per
-        return per * self.passes + (self._nin if self.planes_mode else 0)
-
-    def _factor_slices(self, mode, factors, stream):
-        """Per input mode and pass: (pointer, row pitch) of the pass's columns.
-        Planes: one skrp_split_columns launch per input mode per call (the
-        factors change every mode in a chained run)."""
-        P, R = self.passes, self.rank
-        w_ = R // P
-        out = {}
-        for w, f in enumerate(factors):
-            if w == mode:
-                continue
-            if not self.planes_mode:
-                out[w] = [(f.data_ptr() + p * w_ * 4, R) for p in range(P)]
-                continue
-            buf = self._planes.get(w)
-            if buf is None or buf.shape[1] != f.shape[0]:
-                buf = _torch().empty((P, f.shape[0], w_), dtype=torch_float32(), device=f.device)
-                self._planes[w] = buf
-            _lib.call("skrp_split_columns", f.data_ptr(), f.shape[0], R, P, buf.data_ptr(), stream)
-            out[w] = [(buf[p].data_ptr(), w_) for p in range(P)]
-        return out
+        return sum(1 + len(sg["levels"]) for sg in self.segments)
 
     def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
         """Launch the tile kernel(s) (+ carry trees).  `events` (start, end) CUDA
@@ -548,39 +504,12 @@ class _ShardExec:
         a.persistent_ctas = 0
         a.variant = cfg.kernel_variant
         a.flags = self.flags
-        if self.rle is not None:
-            a.rle_chg, a.rle_pre, a.rle_runs = (t.data_ptr() for t in self.rle)
 
         if events is not None:
             events[0].record()  # current stream == `stream` (callers launch on it)
-        if self.passes > 1:
-            sl = self._factor_slices(mode, factors, stream)
-            w_ = self.rank // self.passes
-            a.rank = w_
-            a.out_ld = self.rank
-            for p in range(self.passes):
-                for w, lst in sl.items():
-                    a.factors[w] = lst[p][0]
-                    a.factor_ld = lst[p][1]
-                a.out = out.data_ptr() + p * w_ * 4
-                for seg in self.segments:
-                    a.tiles = seg["tiles"].data_ptr()
-                    a.num_tiles = seg["n"]
-                    _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
-            if events is not None:
-                events[1].record()
-            return
         for seg in self.segments:
             a.tiles = seg["tiles"].data_ptr()
             a.num_tiles = seg["n"]
-            if self.window is not None and seg["key"] is not None:
-                w, shift = self.window
-                rows = 1 << shift
-                lo = seg["key"] * rows
-                n_rows = max(0, min(rows, factors[w].shape[0] - lo))
-                a.l2_window_base = factors[w].data_ptr() + lo * self.rank * 4
-                a.l2_window_bytes = n_rows * self.rank * 4
-                a.l2_window_hit_ratio = 1.0
             _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), stream), "skrp_mttkrp_tiles")
             if not self.det:
                 continue
@@ -780,7 +709,7 @@ class _PanelExec:
         pa.groups = self.groups
         pa.slab_rows = self.slab_rows
         pa.warps = self.warps
-        pa.flags = (_lib.PANEL_LOCKSTEP if self.lockstep else 0) | (_lib.PANEL_GROUP_SYNC if cfg.panel_group_sync else 0)
+        pa.flags = _lib.PANEL_LOCKSTEP if self.lockstep else 0
         if peers is not None and peers[1]:
             pa.peer_out = peers[0].data_ptr()
             pa.num_peers = peers[1]
@@ -789,91 +718,6 @@ class _PanelExec:
         _lib.check(_lib.lib().skrp_mttkrp_panels(ctypes.byref(a), ctypes.byref(pa), stream), "skrp_mttkrp_panels")
         if events is not None:
             events[1].record()
-
-
-class _SlotExec:
-    """Item / slot tables of the slot-owned panel kernel (plan.to_slots) for a
-    set of shards: one launch per mode, every owned row written exactly once
-    (no output zeroing), bit-identical for any placement (DESIGN.md §4 K1c)."""
-
-    writes_all_rows = True
-
-    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
-        torch = _torch()
-        sl = plan.slots
-        self.gpu = gpu
-        self.rank = rank
-        self.det = True
-        self.passes = 1
-        self.levels = []
-        self.tile_nnz = 0
-        mine = np.isin(sl["item_shard"], np.asarray(list(shard_ids), dtype=np.int64))
-        idx = np.nonzero(mine)[0]
-        self.num_items = int(len(idx))
-        self.num_tiles = self.num_items
-        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
-        self.item_rows = torch.from_numpy(np.ascontiguousarray(sl["item_rows"][idx])).to(gpu)
-        ti = torch.from_numpy(idx).to(sl["slot_offsets"].device)
-        self.slot_offsets = sl["slot_offsets"].index_select(0, ti).to(gpu).contiguous()
-        self.nslot, self.rps = sl["nslot"], sl["rps"]
-        self.shifts = sl["shifts"]
-        self.counter = torch.zeros(1, dtype=torch.int32, device=gpu)
-
-    @property
-    def launches(self) -> int:
-        return 1 if self.num_items else 0
-
-    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None,
-            peers=None):
-        if self.num_items == 0:
-            return
-        a = _lib.MttkrpArgs()
-        a.nmodes = len(coords)
-        a.mode = mode
-        a.rank = self.rank
-        a.accumulation = _lib.ACC_DETERMINISTIC
-        a.nnz = nnz_total
-        for w, c in enumerate(coords):
-            a.coords[w] = c.data_ptr()
-            a.factors[w] = None if w == mode else factors[w].data_ptr()
-        a.values = vals.data_ptr()
-        a.out = out.data_ptr()
-        sa = _lib.SlotArgs()
-        sa.item_rows = self.item_rows.data_ptr()
-        sa.slot_offsets = self.slot_offsets.data_ptr()
-        sa.num_items = self.num_items
-        sa.slots_per_item = self.nslot
-        sa.rows_per_slot = self.rps
-        sa.tile_shift0, sa.tile_shift1 = self.shifts
-        sa.round_counter = self.counter.data_ptr()
-        if peers is not None and peers[1]:
-            sa.peer_out = peers[0].data_ptr()
-            sa.num_peers = peers[1]
-        if events is not None:
-            events[0].record()
-        _lib.check(_lib.lib().skrp_mttkrp_slots(ctypes.byref(a), ctypes.byref(sa), stream), "skrp_mttkrp_slots")
-        if events is not None:
-            events[1].record()
-
-
-def slot_blocking(plan, rank, block_mb=32, shift=0):
-    """Block shifts of the slot layout: every input factor larger than one
-    block is cut into `block_mb` blocks (2^18 rows at R = 32), the others stay
-    whole (a tile = one block of each input, L2-resident while every SM works
-    on it)."""
-    if shift <= 0:
-        rows = max(1, (block_mb << 20) // (rank * 4))
-        shift = max(0, rows.bit_length() - 1)
-    return [shift if (w != plan.mode and plan.shape[w] > (1 << shift)) else -1 for w in range(len(plan.shape))]
-
-
-def slots_apply(plan, rank) -> bool:
-    """The slot kernel applies: N = 3, R = 32, no row heavier than a slot can
-    carry alone, and inputs too large to stay L2-resident unblocked."""
-    if len(plan.shape) != 3 or rank != 32:
-        return False
-    ins = [w for w in range(3) if w != plan.mode]
-    return sum(plan.shape[w] * rank * 4 for w in ins) > (96 << 20)
 
 
 def panel_shape(nmodes: int, rank: int):
@@ -944,10 +788,6 @@ def choose_panels(plan, rank, cfg: PlatformConfig, shard_ids=None):
     return (slab_shift, shifts, warps)
 
 
-def torch_float32():
-    return _torch().float32
-
-
 def _plan_arrays(plan: ModePartitionPlan, gpu):
     """The plan's sorted arrays on `gpu` (copied once and cached if the plan
     was built on another GPU); host-resident (out-of-core) plans are returned
@@ -964,49 +804,15 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
     return plan._exec_cache[key]
 
 
-def _plan_rle(plan, gpu):
-    """Run-length form of the plan's output-row ids on `gpu` (cached with the
-    layout): (change bits, per-word run prefix, run ids) for
-    skrp_mttkrp_args.rle_* -- ~0.35 B per nonzero instead of 4 at cfg2."""
-    key = ("rle", str(gpu))
-    got = plan._exec_cache.get(key)
-    if got is not None:
-        return got
-    torch = _torch()
-    from .distplan import _prefix
-
-    coords, _ = _plan_arrays(plan, gpu)
-    rows, n = coords[plan.mode], int(plan.nnz)
-    words = n // 32 + 2
-    stream = torch.cuda.current_stream(gpu).cuda_stream
-    with torch.cuda.device(gpu):
-        chg = torch.empty(words, dtype=torch.int32, device=gpu)
-        counts = torch.empty(words, dtype=torch.int64, device=gpu)
-        _lib.call("skrp_rle_mark", rows.data_ptr(), n, chg.data_ptr(), counts.data_ptr(), stream)
-        prefix = _prefix(counts, stream)
-        del counts
-        runs = torch.empty(max(1, int(prefix[-1].item())), dtype=torch.int32, device=gpu)
-        pre = torch.empty(words, dtype=torch.int32, device=gpu)
-        _lib.call("skrp_rle_runs", rows.data_ptr(), n, chg.data_ptr(), prefix.data_ptr(), pre.data_ptr(),
-                  runs.data_ptr(), stream)
-    got = (chg, pre, runs)
-    plan._exec_cache[key] = got
-    return got
-
-
 def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
     key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout,
-           clip, cfg.col_passes, cfg.col_planes, cfg.l2_window_mb, cfg.rle_rows)
+           clip)
     ex = plan._exec_cache.get(key)
     if ex is None:
         if plan.layout == "panel":
             if clip is not None:
                 raise ValueError("element-split placement needs the plan-order (flycoo) layout")
             ex = _PanelExec(plan, shard_ids, cfg, rank, gpu)
-        elif plan.layout == "slots":
-            if clip is not None:
-                raise ValueError("element-split placement needs the plan-order (flycoo) layout")
-            ex = _SlotExec(plan, shard_ids, cfg, rank, gpu)
         elif plan.layout == "host":
             if clip is not None:
                 raise ValueError("element-split placement is not streamed")
@@ -1095,6 +901,7 @@ def mttkrp_mode(plan: ModePartitionPlan, devices: list, cfg: PlatformConfig,
         assignment = assign_shards(plan, m, cfg.scheduling)
     apply_layout(plan, cfg, rank)
 
+    torch.cuda.nvtx.range_push(f"skrp mttkrp_mode {mode}")
     events = []
     for dev in devices:
         dev.reset_for_mode(rows, rank, collect_write_log=collect_write_log)
@@ -1143,10 +950,17 @@ def mttkrp_mode(plan: ModePartitionPlan, devices: list, cfg: PlatformConfig,
         allgather_seconds=allgather_seconds,
         barrier_count=2,
         wall_seconds=time.perf_counter() - t_mode,
+        algorithmic_bytes=plan.nnz * (4 * len(plan.shape) + 4) + plan.nnz * (len(plan.shape) - 1) * rank * 4
+        + rows * rank * 4,
     )
+    torch.cuda.nvtx.range_pop()
     out = devices[0].output
     if as_numpy:
-        return out.double().cpu().numpy(), metrics
+        from .hostio import ExportQueue
+
+        q = ExportQueue(out.device)
+        q.push(out)
+        return q.results()[0], metrics
     return out, metrics
 
 
@@ -1159,11 +973,22 @@ def mttkrp_all_modes(plans: list, devices: list, cfg: PlatformConfig, ledger: Tr
     metrics.preprocessing_seconds = [p.build_time for p in plans]
     outputs = []
     t0 = time.perf_counter()
+    export = None
+    if as_numpy and devices:
+        # each mode's float64 copy leaves on a side stream while the next
+        # modes compute (hostio.ExportQueue), not after the last one
+        from .hostio import ExportQueue
+
+        export = ExportQueue(devices[0].cuda_device)
     for plan in plans:
         out, mm = mttkrp_mode(plan, devices, cfg, ledger, update_factors=True,
-                              collect_write_log=collect_write_log, as_numpy=as_numpy)
+                              collect_write_log=collect_write_log, as_numpy=False)
+        if export is not None:
+            export.push(out)
         outputs.append(out)
         metrics.modes.append(mm)
+    if export is not None:
+        outputs = export.results()
     metrics.wall_seconds = time.perf_counter() - t0
     return outputs, metrics
 

@@ -146,7 +146,6 @@ class ModePartitionPlan:
         self.block_order = None
         self.groups = None
         self.panel = None
-        self.slots = None
         self.shards = [
             TensorShard(self, mode, j, (int(self.bounds[j]), int(self.bounds[j + 1])),
                         int(self.offsets[j]), int(self.offsets[j + 1]),
@@ -410,111 +409,6 @@ class ModePartitionPlan:
         self._exec_cache.clear()
         torch.cuda.current_stream(dev).synchronize()
         return self
-
-    def to_slots(self, shifts):
-        """Reorder the device arrays IN PLACE into the SLOT layout of the
-        slot-owned panel kernel (csrc/mttkrp_slots.cu; N = 3, R = 32).
-
-        ITEM = the part of one output slab of P = slots x rows_per_slot rows
-        inside one shard (slabs start at the shard's first row); slot s of an
-        item owns its rows [s*rps, (s+1)*rps).  Key = [item | slot | tile],
-        tile = (c_in0 >> shifts[in0], c_in1 >> shifts[in1]) (-1: unblocked),
-        stable -- so a slot's nonzeros are contiguous, ordered by tile and,
-        inside a tile, by row in plan order.  ``self.slots`` holds the item
-        rows, shards and per-item slot offsets.  The new arrays carry
-        chunk_slack readable elements past the end (the kernel's aligned TMA
-        windows).  Shard offsets and host-visible plan views are unchanged."""
-        import ctypes
-
-        import torch
-
-        if self.layout != "flycoo":
-            raise ValueError("plan is already in a reordered layout")
-        n, d = len(self.shape), self.mode
-        if n != 3:
-            raise ValueError("slot layout: 3-mode tensors only")
-        nslot, rps, slack = (ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32())
-        _lib.call("skrp_slots_shape", 3, 32, ctypes.byref(nslot), ctypes.byref(rps), ctypes.byref(slack))
-        nslot, rps, slack = nslot.value, rps.value, slack.value
-        P = nslot * rps
-        ins = [w for w in range(3) if w != d]
-        shifts = [int(x) for x in shifts]
-        sh = [shifts[w] if shifts[w] >= 0 else 31 for w in ins]
-        tb = [max(0, _key_bits(-(-self.shape[w] // (1 << sh[i])))) if sh[i] < 31 else 0 for i, w in enumerate(ins)]
-        rows_items, item_shard = [], []
-        for j, shd in enumerate(self.shards):
-            lo, hi = shd.index_range
-            for r0 in range(lo, hi, P):
-                rows_items.append((r0, min(r0 + P, hi)))
-                item_shard.append(j)
-        n_items = len(rows_items)
-        slot_bits = _key_bits(nslot)
-        item_bits = max(1, _key_bits(max(n_items, 1)))
-        low = tb[0] + tb[1]
-        total = item_bits + slot_bits + low
-        if total > 31:
-            raise ValueError(f"slot key needs {total} > 31 bits (coarser blocks or fewer items)")
-        dev = self.vals.device
-        stream = torch.cuda.current_stream(dev).cuda_stream
-        nnz = self.nnz
-        starts = torch.tensor([r[0] for r in rows_items] or [0], dtype=torch.int64, device=dev)
-        rows_all = torch.arange(self.shape[d], dtype=torch.int64, device=dev)
-        item_of = torch.searchsorted(starts, rows_all, right=True) - 1
-        prefix = (((item_of << slot_bits) | ((rows_all - starts[item_of]) // rps)) << low).to(torch.int32)
-        del rows_all, item_of
-        keys = torch.empty(nnz, dtype=torch.int32, device=dev)
-        _lib.call("skrp_slot_keys", self.coords[d].data_ptr(), self.coords[ins[0]].data_ptr(),
-                  self.coords[ins[1]].data_ptr(), nnz, prefix.data_ptr(), sh[0], sh[1], tb[1], keys.data_ptr(),
-                  stream)
-        del prefix
-        sorted_keys = self._permute_by_keys(keys, total, slack)
-        del keys
-        q = (torch.arange(n_items, dtype=torch.int64, device=dev)[:, None] << slot_bits) \
-            + torch.arange(nslot + 1, dtype=torch.int64, device=dev)[None, :]
-        q = (q << low).to(torch.int32)  # slot nslot of item i == slot 0 of item i + 1 (the end)
-        offs = torch.searchsorted(sorted_keys, q.reshape(-1)).reshape(n_items, nslot + 1).to(torch.int64)
-        del sorted_keys
-        self.slots = {
-            "item_rows": np.asarray(rows_items, dtype=np.int64).reshape(-1, 2),
-            "item_shard": np.asarray(item_shard, dtype=np.int64),
-            "slot_offsets": offs.contiguous(),
-            "shifts": tuple(sh), "nslot": nslot, "rps": rps,
-        }
-        self.layout = "slots"
-        self.block_shifts = shifts
-        self.block_order = ins
-        self.groups = None
-        self._exec_cache.clear()
-        torch.cuda.current_stream(dev).synchronize()
-        return self
-
-    def _permute_by_keys(self, keys, total_bits, slack=0):
-        """Stable sort of the device arrays by ``keys`` (int32, total_bits
-        wide); new arrays get ``slack`` readable elements past nnz.  Keeps
-        ``exec_perm`` like _reorder_by_key.  Returns the sorted keys."""
-        import torch
-
-        nnz = self.nnz
-        dev = self.vals.device
-        stream = torch.cuda.current_stream(dev).cuda_stream
-        sorted_keys = torch.empty_like(keys)
-        perm = torch.empty_like(keys)
-        ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, total_bits)
-        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
-        _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), nnz, total_bits, sorted_keys.data_ptr(),
-                  perm.data_ptr(), ws.data_ptr(), ws_bytes, stream)
-        del ws
-
-        def permuted(src):
-            buf = torch.zeros(nnz + slack, dtype=src.dtype, device=dev)
-            _lib.call("skrp_gather_u32", src.data_ptr(), perm.data_ptr(), nnz, buf.data_ptr(), stream)
-            return buf[:nnz]
-
-        for w in range(len(self.shape)):
-            self.coords[w] = permuted(self.coords[w])
-        self.vals = permuted(self.vals)
-        self.exec_perm = perm if self.perm is not None else None
-        return sorted_keys
 
     def to_host(self):
         """Out-of-core execution (the B200 form of the

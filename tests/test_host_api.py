@@ -239,6 +239,11 @@ def test_metrics_schema():
     recs = sk.run_records(rm, platform=sk.PlatformConfig(devices=2))
     assert [r["record"] for r in recs] == ["platform", "preprocessing", "device_compute", "device_compute",
                                            "mode_summary", "imbalance", "totals"]
+    # B200 additions: throughput over the critical path, algorithmic-bytes roofline
+    mm.algorithmic_bytes = 6_000_000_000
+    assert rm.nnz_per_s == 4.0 and mm.nnz_per_s == 4.0 and mm.compute_seconds == 3.0
+    roof = rm.roofline(1000.0)
+    assert roof["achieved_gbs"] == 2.0 and roof["frac_algorithmic"] == 0.002 and roof["nnz_per_s"] == 4.0
 
 
 def test_elementwise_compute_spec():
@@ -425,10 +430,6 @@ def test_spec_acceptance_imbalance():
 def test_device_entry_points_validate_before_launch():
     """Argument checks of device entry points run on the host before any CUDA
     call: bad sizes map to ValueError with the entry point named (no GPU)."""
-    with pytest.raises(ValueError, match="skrp_rle_mark"):
-        _lib.call("skrp_rle_mark", None, 1 << 32, None, None, None)
-    with pytest.raises(ValueError, match="skrp_rle_runs"):
-        _lib.call("skrp_rle_runs", None, -1, None, None, None, None, None)
     with pytest.raises(ValueError, match="multiple of 16"):
         _lib.call("skrp_crc32_chunks", None, 100, 10, None, None)
     with pytest.raises(ValueError, match="skrp_plan_unpack_indices"):

@@ -47,13 +47,8 @@ def main():
     fh = open(args.out, "a") if args.out else None
     cache_key = None
     plan = None
-    from paper_2507_15121_b200 import _lib
-    import ctypes
-
     for sp in specs:
         d = sp["mode"]
-        got = ctypes.c_int64()
-        _lib.call("skrp_set_l2_persisting", int(sp.get("persist_mb", 0)) << 20, ctypes.byref(got))
         key = (d, sp.get("layout"), sp.get("slab_shift"), tuple(sp.get("shifts") or []), tuple(sp.get("order") or []),
                json.dumps(sp.get("sweep")), sp.get("warps"))
         if key != cache_key:
@@ -63,7 +58,7 @@ def main():
             plan = sk.build_mode_plan(t, d, pcfg, keep_permutation=False)
             t0 = time.perf_counter()
             if sp.get("layout") == "panel":
-                warps = sp.get("warps") or panel_shape(len(shape), R // sp.get("passes", 1))[0]
+                warps = sp.get("warps") or panel_shape(len(shape), R)[0]
                 plan.to_panels(sp["slab_shift"], sp["shifts"], warps, sp.get("order"),
                                sweep={int(k): v for k, v in (sp.get("sweep") or {}).items()})
             elif sp.get("shifts"):
@@ -71,9 +66,7 @@ def main():
             block_s = time.perf_counter() - t0
             cache_key = key
         pl = sk.PlatformConfig(devices=1, rank=R, accumulation=sp.get("acc", "atomic"), tile_nnz=sp.get("tile", 0),
-                               kernel_variant=sp.get("variant", 0), col_passes=sp.get("passes", 1),
-                               col_planes=sp.get("planes", True), panel_lockstep=sp.get("lockstep", True),
-                               l2_window_mb=sp.get("window_mb", 0))
+                               kernel_variant=sp.get("variant", 0), panel_lockstep=sp.get("lockstep", True))
         if plan.layout == "panel":
             ex = _PanelExec(plan, list(range(plan.shard_count)), pl, R, dev)
         else:
@@ -96,7 +89,7 @@ def main():
         rec = dict(sp, ms=ms, ms_all=times, groups=(int(sum(len(x) for x in plan.groups)) if plan.groups else
                            (plan.panel["groups"] if plan.layout == "panel" else 0)),
                    tiles=ex.num_tiles, tile_nnz=ex.tile_nnz, frac_alg=alg / (ms * 1e-3) / 6457.4e9,
-                   block_s=block_s, persist_granted=got.value, checksum=float(out.double().sum().item()))
+                   block_s=block_s, checksum=float(out.double().sum().item()))
         line = json.dumps(rec)
         print(line, flush=True)
         if fh:

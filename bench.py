@@ -61,7 +61,7 @@ CONFIGS = {
                   desc="cfg4 Reddit-shaped 8.2Mx177Kx8.1M Zipf(1.2), R=32, all modes, 0.5B nnz (of 4.7B)"),
     # full multi-GPU configs (distributed plan build; one GPU cannot hold them)
     "cfg3": dict(shape=(46, 240_000, 240_000), nnz=3_600_000_000, rank=32, dist="uniform",
-                 strategy="equal-index", modes=None, host_gen=False, dist_build=True,
+                 strategy="equal-index", modes=None, host_gen=False, dist_build=True, park_plans=True,
                  desc="cfg3 Patents-shaped 46x240Kx240K, 3.6B nnz uniform, R=32, all modes"),
     "cfg4": dict(shape=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, rank=32, dist="zipf",
                  strategy="nnz-balanced", modes=None, host_gen=False, dist_build=True,
@@ -132,7 +132,7 @@ def kernel_key(name):
         n = n[5:]
     for ns in ("skrp::", "(anonymous namespace)::", "::"):
         n = n.replace(ns, "")
-    return n.replace(" ", "").replace("const", "")
+    return n.replace("(int)", "").replace(" ", "").replace("const", "")
 
 
 def lookup_traffic(config, mode, kernel):
@@ -534,9 +534,10 @@ def run_ours(args, cfg):
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
     verify = rank == 0 and not dist_build and not args.no_parity and not args.stream_modes and not args.emulate_world
     plan_checks = []
+    samples = None
     if verify:
-        from oracle.scale import sample_parity_source, verify_plan_full
-    if world == 1 and cfg.get("dist_build", False):
+        from oracle.scale import extract_row_samples, sample_parity_extracted, verify_plan_full
+    if world == 1 and cfg.get("dist_build", False) and not cfg.get("park_plans", False):
         raise SystemExit(f"{args.config} does not fit one B200 ({nnz} nnz); run it with torchrun --nproc-per-node >= 2 "
                          f"or use the single-GPU '{args.config}s' variant")
     if dist_build:
@@ -552,6 +553,10 @@ def run_ours(args, cfg):
             tensor = sk.synth_tensor(shape, nnz, distribution=cfg["dist"], seed=0)
         else:
             tensor = sk.synth_tensor_device(shape, nnz, distribution=cfg["dist"], seed=0)
+        # full-size cfg3 on one GPU: 3 plans x 57.6 GB fit HBM only without the
+        # source tensor and the sort workspace, so finished plans wait in host
+        # memory while the next mode sorts, and come back once the source is gone
+        park = world == 1 and cfg.get("park_plans", False)
         plans = []
         for d in modes:
             p_ = sk.build_mode_plan(tensor, d, pcfg, keep_permutation=verify)
@@ -561,12 +566,25 @@ def run_ours(args, cfg):
                 src_c, src_v = tensor.device_arrays()
                 plan_checks.append(verify_plan_full(src_c, src_v, p_, cfg["strategy"], devices=pcfg.devices,
                                                     isp_capacity=pcfg.isp_capacity))
+                del src_c, src_v
                 p_.perm = None
-                torch.cuda.empty_cache()
+            if park and d != modes[-1]:
+                p_.to_host(pinned=False)
+            torch.cuda.empty_cache()
             plans.append(p_)
+        if verify:
+            # the sampled rows' source nonzeros go to the host now, so the source
+            # can leave HBM before the run (phase 2 after the run)
+            src_c, src_v = tensor.device_arrays()
+            samples = extract_row_samples(src_c, src_v, shape, modes, rows_per_mode=args.parity_rows)
+            del src_c, src_v
+        if cfg.get("kind") != "cpd" or not verify:
+            tensor.drop_device()  # (CP-ALS parity reads the source during its checked iteration)
+        torch.cuda.empty_cache()
+        for p_ in plans:
+            if p_.layout == "host":
+                p_.to_device()
     build_s = [p.build_time for p in plans]
-    if not verify:
-        tensor.drop_device()  # (kept for the source-tensor parity sample otherwise)
     torch.cuda.empty_cache()
     init = sk.random_factors(shape, R, seed=0)
     host_f = [torch.from_numpy(f.data.astype(np.float32)).pin_memory() for f in init]
@@ -716,12 +734,9 @@ def run_ours(args, cfg):
     # ---- parity on a seeded sample of output rows (chained replay, fp64)
     parity = None
     if verify:
-        src_c, src_v = tensor.device_arrays()
-        parity = sample_parity_source(src_c, src_v, shape, [f.data for f in init], runner.outputs, modes,
-                                      rows_per_mode=args.parity_rows)
+        parity = sample_parity_extracted(samples, [f.data for f in init], runner.outputs)
         parity["plans"] = plan_checks
         parity["plans_ok"] = all(c["ok"] for c in plan_checks)
-        tensor.drop_device()
     elif rank == 0 and not args.no_parity and not streamed:
         # distributed build: no rank holds the source tensor; rows owned here are
         # recomputed from this rank's plan arrays

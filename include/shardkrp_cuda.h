@@ -260,7 +260,7 @@ int skrp_synth_values(float *out, int64_t n, int32_t normal, uint64_t seed, int6
                       skrp_stream_t stream);
 /* keep[i] = 1 iff element i is the first occurrence of its coordinate tuple
  * (synth.py:68-84 dedup rule).  table: caller scratch of table_slots uint64
- * (power of two >= 2n). */
+ * (power of two >= 1.5 n: load factor <= 2/3). */
 int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int64_t n, void *table,
                     int64_t table_slots, uint8_t *keep, skrp_stream_t stream);
 

@@ -105,55 +105,85 @@ def verify_plan_full(src_coords, src_vals, plan, strategy, oversubscription=4, d
     return res
 
 
-def sample_parity_source(src_coords, src_vals, shape, init_factors, outputs, modes, rows_per_mode=4096, seed=0,
-                         nnz_budget=8_000_000, tol=1e-4):
-    """Sampled-row parity against the source tensor (see module docstring).
-    init_factors: fp64 numpy arrays; outputs: the GPU's per-mode outputs
-    (torch, any float dtype, I_d x R) in `modes` order."""
+def extract_row_samples(src_coords, src_vals, shape, modes, rows_per_mode=4096, seed=0, nnz_budget=8_000_000):
+    """Phase 1 of the sampled-row parity: for every mode, a seeded sample of
+    output rows (rows added while their nonzeros fit `nnz_budget`; at least
+    one) and ALL their nonzeros from the SOURCE tensor, copied to host memory
+    (so the source can be freed before the run -- full-size cfg3 on one GPU).
+    Returns one dict per mode: rows (int64), coords (n x N int64), vals (f64)."""
+    import torch
+
+    dev = src_vals.device
+    rng = np.random.default_rng(seed)
+    out = []
+    for d in modes:
+        col = src_coords[d]
+        cand = np.sort(rng.permutation(shape[d])[:rows_per_mode]).astype(np.int64)
+        counts = source_histogram(col, shape[d]).index_select(0, torch.from_numpy(cand).to(dev)).cpu().numpy()
+        keep, tot = [], 0
+        for r, n in zip(cand, counts):
+            if tot + n <= nnz_budget or not keep:
+                keep.append(r)
+                tot += int(n)
+        rows = np.asarray(keep, dtype=np.int64)
+        member = torch.zeros(shape[d], dtype=torch.bool, device=dev)
+        member[torch.from_numpy(rows).to(dev)] = True
+        sel_all = []
+        for a in range(0, col.numel(), _CHUNK):
+            sel = member[_u32(col[a:a + _CHUNK])].nonzero().squeeze(1)
+            if sel.numel():
+                sel_all.append(sel + a)
+        sel = torch.cat(sel_all) if sel_all else torch.zeros(0, dtype=torch.int64, device=dev)
+        coords = torch.stack([_u32(c.index_select(0, sel)) for c in src_coords], 1).cpu().numpy()
+        vals = src_vals.index_select(0, sel).double().cpu().numpy()
+        out.append({"mode": d, "rows": rows, "coords": coords, "vals": vals})
+    return out
+
+
+def sample_parity_extracted(samples, init_factors, outputs, tol=1e-4):
+    """Phase 2: max |gpu - ref| / max(|ref|, 1) (cli.py:247-261) over the
+    sampled rows, ref = fp64 MTTKRP of their source nonzeros with the chained
+    factors (mode d reads the GPU's own outputs of the modes before it, as the
+    reference's mttkrp_all_modes does).  fp64 arithmetic in torch on the
+    outputs' GPU (checker only).  outputs: the GPU's per-mode outputs in the
+    order of `samples`."""
     import torch
 
     dev = outputs[0].device
     facs = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).to(dev) for f in init_factors]
     rank = facs[0].shape[1]
-    rng = np.random.default_rng(seed)
     worst, checked, per_mode = 0.0, 0, []
-    for i, d in enumerate(modes):
-        col = src_coords[d]
-        cand = np.sort(rng.permutation(shape[d])[:rows_per_mode]).astype(np.int64)
-        rows_t = torch.from_numpy(cand).to(dev)
-        counts = source_histogram(col, shape[d]).index_select(0, rows_t).cpu().numpy()
-        keep, tot = [], 0
-        for r, n in zip(cand, counts):  # rows in the budget (at least one)
-            if tot + n <= nnz_budget or not keep:
-                keep.append(r)
-                tot += int(n)
-        rows = np.asarray(keep, dtype=np.int64)
-        rows_t = torch.from_numpy(rows).to(dev)
-        member = torch.zeros(shape[d], dtype=torch.bool, device=dev)
-        member[rows_t] = True
-        expect = torch.zeros((len(rows), rank), dtype=torch.float64, device=dev)
-        for a in range(0, col.numel(), _CHUNK):
-            c = _u32(col[a:a + _CHUNK])
-            sel = member[c].nonzero().squeeze(1)
-            if sel.numel() == 0:
-                continue
-            s_ = sel + a
-            contrib = src_vals.index_select(0, s_).double()[:, None].expand(-1, rank).clone()
-            for w in range(len(shape)):
+    for i, smp in enumerate(samples):
+        d = smp["mode"]
+        rows_t = torch.from_numpy(smp["rows"]).to(dev)
+        expect = torch.zeros((rows_t.numel(), rank), dtype=torch.float64, device=dev)
+        nsel = smp["coords"].shape[0]
+        for a in range(0, nsel, 1 << 22):  # bounded temporaries (a head row can hold 10^8 nonzeros)
+            coords = torch.from_numpy(smp["coords"][a:a + (1 << 22)]).to(dev)
+            contrib = torch.from_numpy(smp["vals"][a:a + (1 << 22)]).to(dev)[:, None].expand(-1, rank).clone()
+            for w in range(coords.shape[1]):
                 if w != d:
-                    contrib *= facs[w].index_select(0, _u32(src_coords[w].index_select(0, s_)))
-            pos = torch.searchsorted(rows_t, _u32(col.index_select(0, s_)))
-            expect.index_add_(0, pos, contrib)
+                    contrib *= facs[w].index_select(0, coords[:, w])
+            expect.index_add_(0, torch.searchsorted(rows_t, coords[:, d]), contrib)
+            del coords, contrib
         got = outputs[i].index_select(0, rows_t).double()
-        err = float(((got - expect).abs() / expect.abs().clamp(min=1.0)).max().item()) if len(rows) else 0.0
-        per_mode.append({"mode": d, "rows": int(len(rows)), "nnz": int(tot), "max_rel_err": err})
+        err = float(((got - expect).abs() / expect.abs().clamp(min=1.0)).max().item()) if rows_t.numel() else 0.0
+        per_mode.append({"mode": d, "rows": int(rows_t.numel()), "nnz": int(nsel), "max_rel_err": err})
         worst = max(worst, err)
-        checked += len(rows)
+        checked += int(rows_t.numel())
         facs[d] = outputs[i].double()
     return {"rows_checked": checked, "max_rel_err": worst, "tolerance": tol, "ok": worst <= tol,
             "per_mode": per_mode,
-            "method": "seeded output-row sample; fp64 recomputation from the SOURCE tensor (generator arrays, "
-                      "not the plan), chained factors; torch on the GPU as checker (oracle/scale.py)"}
+            "method": "seeded output-row sample; fp64 recomputation from the SOURCE tensor's nonzeros of those "
+                      "rows (generator arrays, not the plan), chained factors; torch on the GPU as checker "
+                      "(oracle/scale.py)"}
+
+
+def sample_parity_source(src_coords, src_vals, shape, init_factors, outputs, modes, rows_per_mode=4096, seed=0,
+                         nnz_budget=8_000_000, tol=1e-4):
+    """Both phases at once (source still on the device)."""
+    samples = extract_row_samples(src_coords, src_vals, shape, modes, rows_per_mode, seed, nnz_budget)
+    return sample_parity_extracted(samples, init_factors, outputs, tol)
 
 
 def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_per_mode=1024, seed=0,
@@ -164,7 +194,9 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
     Expected, in fp64 from the SOURCE tensor: M[rows] (MTTKRP), and
     M[rows] @ V^-1 with V = Hadamard of the other modes' Grams (computed here
     in fp64 from facs) applied to the GPU's own M rows -- compared with
-    new[rows] * lambdas (the GPU's update before normalisation).  Returns
+    new[rows] * lambdas (the GPU's update before normalisation), the error
+    scaled by sum_k |M_k| |W_kj| (the bound of a dot product in finite
+    precision: the update is checked to working accuracy).  Returns
     {max_rel_err_mttkrp, max_rel_err_update, ...}; the update error against a
     fully fp64 chain and cond(V) are reported alongside."""
     import torch
@@ -203,9 +235,15 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
             v *= f64[w].T @ f64[w]
     lam = torch.from_numpy(np.asarray(lambdas, dtype=np.float64)).to(dev)
     got_u = new.index_select(0, rows_t).double() * lam[None, :]
-    # the update step itself: fp64 M_gpu V^-1 from the GPU's own M (V symmetric)
-    upd = torch.linalg.solve(v, got_m.T).T
-    err_u = float(((got_u - upd).abs() / upd.abs().clamp(min=1.0)).max().item())
+    # the update step itself: fp64 M_gpu V^-1 from the GPU's own M.  V^-1 has
+    # large entries of both signs when V is ill-conditioned, so the result is
+    # a cancelling sum; its error is measured against the scale fp arithmetic
+    # guarantees, sum_k |M_k| |W_kj| (|fl(sum a_k b_k) - sum a_k b_k| <=
+    # gamma_n sum |a_k||b_k|), i.e. the update must be exact to working accuracy
+    w = torch.linalg.inv(v)
+    upd = got_m @ w
+    scale = got_m.abs() @ w.abs()
+    err_u = float(((got_u - upd).abs() / scale.clamp(min=1e-300)).max().item())
     # end to end (info): fp64 M V^-1 from the source -- M's fp32 rounding
     # (err_m) amplified by cond(V), a property of fp32 arithmetic, not gated
     upd64 = torch.linalg.solve(v, expect.T).T

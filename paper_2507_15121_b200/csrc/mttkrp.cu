@@ -25,6 +25,7 @@
 //         the result is bit-identical for any device count, like the
 //         reference's deterministic-reduce, engine.py:12-16).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 

@@ -189,8 +189,8 @@ extern "C" int skrp_dedup_mark(const int32_t *const *coords, int32_t nmodes, int
                                int64_t table_slots, uint8_t *keep, skrp_stream_t stream)
 {
     SKRP_REQUIRE(nmodes >= 1 && nmodes <= SKRP_MAX_MODES && n >= 0, "skrp_dedup_mark: bad sizes");
-    SKRP_REQUIRE(table_slots >= 2 * n && (table_slots & (table_slots - 1)) == 0,
-                 "skrp_dedup_mark: table_slots must be a power of two >= 2n");
+    SKRP_REQUIRE(2 * table_slots >= 3 * n && table_slots > 0 && (table_slots & (table_slots - 1)) == 0,
+                 "skrp_dedup_mark: table_slots must be a power of two >= 1.5 n (load factor <= 2/3)");
     if (n == 0) return SKRP_OK;
     SKRP_REQUIRE(coords && table && keep, "skrp_dedup_mark: null pointer");
     TupleArgs a{};

@@ -410,18 +410,22 @@ class ModePartitionPlan:
         torch.cuda.current_stream(dev).synchronize()
         return self
 
-    def to_host(self):
+    def to_host(self, pinned=True):
         """Out-of-core execution (the B200 form of the
         reference's per-mode staging, engine.py:103-105): move the sorted
         arrays to PINNED host memory and free their HBM; the stream executor
         (engine._StreamExec) copies them back chunk by chunk, overlapped with
-        the kernel, every time the mode runs.  Plan order only."""
+        the kernel, every time the mode runs.  Plan order only.
+        ``pinned=False`` parks the arrays in pageable memory of their exact
+        size (a build parking finished plans; see to_device)."""
         import torch
 
         if self.layout != "flycoo":
             raise ValueError("out-of-core execution streams the plan (FLYCOO) order")
 
         def pin(t):
+            if not pinned:
+                return t.cpu()
             h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             h.copy_(t)
             return h
@@ -431,6 +435,24 @@ class ModePartitionPlan:
         if self.perm is not None:
             self.perm = self.perm.cpu()
         self.layout = "host"
+        self._exec_cache.clear()
+        return self
+
+    def to_device(self, device=None):
+        """Inverse of to_host: the pinned arrays back into HBM (plan order).
+        Lets a build park finished plans on the host while the next mode's
+        sort needs the HBM (full-size cfg3 on one GPU, bench.py)."""
+        import torch
+
+        if self.layout != "host":
+            raise ValueError("plan is not host-resident")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.coords = [c.to(dev, non_blocking=True) for c in self.coords]
+        self.vals = self.vals.to(dev, non_blocking=True)
+        if self.perm is not None:
+            self.perm = self.perm.to(dev)
+        torch.cuda.current_stream(dev).synchronize()
+        self.layout = "flycoo"
         self._exec_cache.clear()
         return self
 

@@ -156,11 +156,16 @@ def synth_tensor_device(shape, nnz, distribution="uniform", zipf_exponent=1.2,
             count = max(short + short // 4 + 16, 64)
             batch = draw(count, drawn)
             drawn += count
-            pool = [torch.cat([c, b]) for c, b in zip(coords, batch)]
+            if coords[0].numel() == 0:  # first round: no copy of the batch
+                pool = batch
+            else:
+                pool = [torch.cat([c, b]) for c, b in zip(coords, batch)]
             del batch
             n = pool[0].numel()
+            # open-addressing table at load factor <= 1/2, or <= 2/3 past 2^31
+            # entries (10^9-scale pools: the table is the largest buffer)
             slots = 1
-            while slots < 2 * n:
+            while slots < (2 * n if n < (1 << 31) else (3 * n) // 2):
                 slots *= 2
             table = torch.empty(slots, dtype=torch.int64, device=dev)
             keep = torch.empty(n, dtype=torch.uint8, device=dev)

@@ -895,7 +895,7 @@ def test_plan_cache_reference_files(golden, tmp_path):
         sk.load_plan(bad)
 
 
-@pytest.mark.parametrize("layout,variant", [("blocked", 0), ("blocked", 1), ("panel", 0)])
+@pytest.mark.parametrize("layout,variant", [("blocked", 0), ("panel", 0)])
 def test_streamed_input_policy_parity(layout, variant):
     """Pin-one-stream-one layouts with factors > 32 MB: the streamed input is
     flagged (SKRP_FLAG_STREAM_INPUTj -> evict_first loads) in the tile and

@@ -439,3 +439,23 @@ def test_device_entry_points_validate_before_launch():
     # zero-length calls are valid no-ops
     _lib.call("skrp_crc32_chunks", None, 0, 16, None, None)
     _lib.call("skrp_f64_to_f32", None, 0, None, None)
+
+
+def test_bench_roofline_matches_exact_kernel():
+    """bench.py reports measured DRAM traffic only for the exact kernel
+    instantiation an ncu capture measured (profiles/ncu_traffic.json): the
+    library's demangled launch-log name and ncu's name normalise alike, a
+    different template instantiation or mode gets no entry."""
+    import bench
+
+    a = bench.kernel_key("void skrp::mttkrp_v2_kernel<(int)3, (int)4, (int)4, (int)2, (int)66, (int)1>"
+                         "(skrp_mttkrp_args, int)")
+    b = bench.kernel_key("void mttkrp_v2_kernel<3, 4, 4, 2, 66, 1>(skrp_mttkrp_args, int)")
+    assert a == b
+    ent, why = bench.lookup_traffic("cfg2", 0, "void skrp::mttkrp_v2_kernel<3, 4, 4, 2, 66, 1>(skrp_mttkrp_args, int)")
+    assert ent is not None and ent["traffic_bytes_per_launch"] > 1e11 and why is None
+    assert ent["source"].startswith("profiles/")
+    ent, why = bench.lookup_traffic("cfg2", 0, "void skrp::mttkrp_v2_kernel<3, 4, 4, 2, 74, 1, 0, 1>(skrp_mttkrp_args, int)")
+    assert ent is None and "no ncu capture" in why
+    ent, _ = bench.lookup_traffic("cfg2", 2, "void skrp::mttkrp_v2_kernel<3, 4, 4, 2, 66, 1>(skrp_mttkrp_args, int)")
+    assert ent is None

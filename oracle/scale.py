@@ -164,7 +164,7 @@ def sample_parity_extracted(samples, init_factors, outputs, tol=1e-4):
             for w in range(coords.shape[1]):
                 if w != d:
                     contrib *= facs[w].index_select(0, coords[:, w])
-            expect.index_add_(0, torch.searchsorted(rows_t, coords[:, d]), contrib)
+            expect.index_add_(0, torch.searchsorted(rows_t, coords[:, d].contiguous()), contrib)
             del coords, contrib
         got = outputs[i].index_select(0, rows_t).double()
         err = float(((got - expect).abs() / expect.abs().clamp(min=1.0)).max().item()) if rows_t.numel() else 0.0

@@ -113,7 +113,7 @@ def plan_balance(plans):
         sizes = getattr(p, "global_shard_nnz", None)
         sizes = np.asarray(sizes if sizes is not None else [s.nnz for s in p.shards], dtype=np.float64)
         out["max_shard_share"].append(float(sizes.max() / max(sizes.sum(), 1)))
-        rows = p.coords[p.mode]
+        rows = p.coords[p.mode] if p.coords is not None else None
         if rows is None or not rows.is_cuda:
             out["max_row_share"].append(None)
             continue
@@ -528,7 +528,9 @@ def run_ours(args, cfg):
                            scheduling=args.scheduling,
                            kernel_variant=args.variant,
                            layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
-                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather)
+                           max_blocks=args.max_blocks, fused_allgather=args.fused_allgather,
+                           cell_lag=args.cell_lag, cell_variant=args.cell_variant, cell_outer_mb=args.cell_outer_mb,
+                           cell_inner_mb=args.cell_inner_mb, cell_keep_arrays=False)
 
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
@@ -1042,7 +1044,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
-    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "auto"))
+    ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "cells", "auto"))
+    ap.add_argument("--cell-lag", type=int, default=0, help="cells layout: lag in cells (0 = free running)")
+    ap.add_argument("--cell-variant", type=int, default=1, help="cells layout: kernel variant (csrc/mttkrp_cells.cu)")
+    ap.add_argument("--cell-outer-mb", type=int, default=32)
+    ap.add_argument("--cell-inner-mb", type=int, default=8)
     ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")

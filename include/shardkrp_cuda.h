@@ -75,7 +75,7 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);
-int skrp_abi_version(void);  /* 11: launch log; A/B-only entry points and fields removed */
+int skrp_abi_version(void);  /* 12: cells execution (skrp_mttkrp_cells) */
 /* Launch log of the MTTKRP kernels, launch order: entry = "<mode>\t<demangled
  * name>" (bench.py matches the kernel it times against the one an ncu
  * capture measured).  index < 0 clears the log; *count receives the number
@@ -191,6 +191,69 @@ int skrp_mttkrp_panels(const skrp_mttkrp_args *args, const skrp_panel_args *pane
  * rank); 0 on success, SKRP_ERR_INVALID when no panel kernel exists. */
 int skrp_panel_shape(int32_t nmodes, int32_t rank, int32_t *warps, int32_t *max_slab_rows);
 
+
+/* GPU-synchronous 2-D blocked execution ("cells", K1d; B200 addition, same
+ * result contract as skrp_mttkrp_tiles for 3-mode tensors): the two input
+ * modes are cut into blocks of 2^outer_shift / 2^inner_shift rows; a CELL is
+ * one (outer block, inner block) pair, numbered in snake order
+ * (cell = bo*inner_blocks + (bo odd ? inner_blocks-1-bi : bi)).  Output rows
+ * [row_lo, row_lo+rows) are cut into STRIPES of stripe_rows rows; stripe s =
+ * (round*ctas + cta)*warps + warp is accumulated by that warp in shared memory
+ * and written once (plain stores: no zeroing needed).  Inside the warp, slot q
+ * (the R/4 lanes of one nonzero; slots = 128/R) processes every slots-th
+ * entry.  `entries` (built by skrp_cell_entries) holds one 16-byte entry
+ * {cell << 20 | stripe-local row * R * 4, outer index, inner index, value bits}
+ * per nonzero plus skip entries: stripe s is entries [stripe_offsets[s],
+ * stripe_offsets[s+1]), cells in order, every cell's part aligned across the
+ * slots (a row's nonzeros in one cell all belong to one slot).
+ * CTAs run cells in step: a warp starts cell c once every CTA finished cell
+ * c-lag (counters in `done`, rounds*cells int32, zeroed by the call; lag <= 0:
+ * no stepping).  Results are bit-identical for any placement of stripes on
+ * devices.  args->coords / values / tiles / carry_* / work_counter are
+ * ignored. */
+typedef struct {
+    int64_t row_lo;                 /* first output row of the layout              */
+    int64_t rows;                   /* output rows covered                         */
+    int64_t out_row_base;           /* global row of args->out[0] (<= row_lo)      */
+    const int64_t *stripe_offsets;  /* stripes + 1 ENTRY offsets (device)          */
+    int64_t stripes;
+    int32_t stripe_rows;
+    int32_t ctas;                   /* CTAs the layout's rounds are cut for (<= #SM) */
+    int32_t outer_mode, inner_mode;
+    int32_t outer_shift, inner_shift;
+    int32_t inner_blocks;
+    int32_t cells;                  /* outer_blocks * inner_blocks, <= 1024          */
+    int32_t lag;
+    int32_t variant;                /* kernel variant the layout was cut for
+                                       (skrp_cell_shape: warps, stage steps)         */
+    int32_t *done;
+    const void *entries;            /* 16-byte entries (device, 16-byte aligned)    */
+} skrp_cell_args;
+
+int skrp_mttkrp_cells(const skrp_mttkrp_args *args, const skrp_cell_args *cells, skrp_stream_t stream);
+/* Variant `variant` of the cells kernel for rank R: warps per CTA, steps per
+ * pipeline ring turn (stripes hold whole turns), largest stripe. */
+int skrp_cell_shape(int32_t rank, int32_t variant, int32_t *warps, int32_t *stage_steps, int32_t *max_stripe_rows);
+/* Layout build (plan.to_cells).  Sort key: keys[i] = (stripe << cell_bits) |
+ * cell, stripe = (rows[i] - row_lo) / stripe_rows.  After a stable sort by it
+ * every (stripe, cell) SEGMENT is contiguous with rows ascending;
+ * skrp_cell_assign gives every run of one row inside a segment to the
+ * least-loaded slot (slot_t[i] = position << 3 | slot, seg_len = longest slot
+ * part) and skrp_cell_entries writes the entries: segment g (= stripe*cells +
+ * cell) occupies [seg_base[g], seg_base[g] + slots*seg_len[g]), entry
+ * t*slots + q = slot q's t-th nonzero; the rest are skip entries carrying the
+ * segment's cell (x = cell << 20 | 0xfffff), stripe tails skip entries of no
+ * cell (x = 0xffffffff).  perm[i] = plan position of sorted position i. */
+int skrp_cell_keys(const uint32_t *rows, const uint32_t *co, const uint32_t *ci, int64_t n, int64_t row_lo,
+                   int32_t stripe_rows, int32_t outer_shift, int32_t inner_shift, int32_t inner_blocks,
+                   int32_t cell_bits, uint32_t *keys, skrp_stream_t stream);
+int skrp_cell_assign(const int64_t *seg_off, int64_t nseg, const uint32_t *rows_sorted, int32_t slots,
+                     uint32_t *slot_t, int32_t *seg_len, skrp_stream_t stream);
+int skrp_cell_entries(const uint32_t *sorted_keys, const uint32_t *perm, const uint32_t *slot_t, int64_t n,
+                      int32_t cell_bits, int32_t cells, const int64_t *seg_base, const int32_t *seg_len, int64_t nseg,
+                      int32_t slots, const uint32_t *rows, const uint32_t *co, const uint32_t *ci, const float *vals,
+                      int64_t row_lo, int32_t stripe_rows, int32_t row_bytes, void *entries, int64_t num_entries,
+                      skrp_stream_t stream);
 
 /* ------------------------------------------------ .tns ingestion (§8(f) 4)
  * GPU restatement of parse_tns (reference tensor.py:173-247).  text: the file

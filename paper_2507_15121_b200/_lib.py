@@ -32,7 +32,7 @@ u64 = ctypes.c_uint64
 sz = ctypes.c_size_t
 
 
-ABI_VERSION = 11  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
+ABI_VERSION = 12  # bumped whenever a struct or signature in include/shardkrp_cuda.h changes
 
 
 class MttkrpArgs(ctypes.Structure):
@@ -75,6 +75,28 @@ class PanelArgs(ctypes.Structure):
     ]
 
 
+class CellArgs(ctypes.Structure):
+    _fields_ = [
+        ("row_lo", i64),
+        ("rows", i64),
+        ("out_row_base", i64),
+        ("stripe_offsets", vp),
+        ("stripes", i64),
+        ("stripe_rows", i32),
+        ("ctas", i32),
+        ("outer_mode", i32),
+        ("inner_mode", i32),
+        ("outer_shift", i32),
+        ("inner_shift", i32),
+        ("inner_blocks", i32),
+        ("cells", i32),
+        ("lag", i32),
+        ("variant", i32),
+        ("done", vp),
+        ("entries", vp),
+    ]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "skrp_last_error": (i32, [ctypes.c_char_p, sz]),
@@ -96,6 +118,12 @@ SIGNATURES = {
     "skrp_tns_parse_token_host": (i32, [ctypes.c_char_p, i64, i32, vp, vp]),
     "skrp_mttkrp_panels": (i32, [vp, vp, vp]),
     "skrp_panel_shape": (i32, [i32, i32, vp, vp]),
+    "skrp_mttkrp_cells": (i32, [vp, vp, vp]),
+    "skrp_cell_shape": (i32, [i32, i32, vp, vp, vp]),
+    "skrp_cell_keys": (i32, [vp, vp, vp, i64, i64, i32, i32, i32, i32, i32, vp, vp]),
+    "skrp_cell_assign": (i32, [vp, i64, vp, i32, vp, vp, vp]),
+    "skrp_cell_entries": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, i64, i32, vp, vp, vp, vp, i64, i32, i32, vp, i64,
+                                vp]),
     "skrp_device_sm_count": (i32, [ctypes.POINTER(i32)]),
     "skrp_histogram": (i32, [vp, i64, i64, vp, vp]),
     "skrp_scan_workspace_bytes": (sz, [i64]),

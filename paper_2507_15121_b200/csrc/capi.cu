@@ -88,7 +88,7 @@ int skrp_last_error(char *buf, size_t len)
     return skrp::g_err_code;
 }
 
-int skrp_abi_version(void) { return 11; }
+int skrp_abi_version(void) { return 12; }
 
 int skrp_device_sm_count(int *out)
 {

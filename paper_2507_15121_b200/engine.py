@@ -71,6 +71,12 @@ class PlatformConfig:
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
+    cell_outer_mb: int = 32     # cells layout: outer input block (MB of factor rows)
+    cell_inner_mb: int = 8      # cells layout: inner input block
+    cell_lag: int = 0           # cells layout: cells a warp may run ahead of the slowest CTA (0 = free running:
+                                #   measured 2-5 % faster on cfg2 -- every warp crosses the cells at the same rate)
+    cell_variant: int = 1       # cells layout: kernel variant (warps per CTA, pipeline depth; see csrc/mttkrp_cells.cu)
+    cell_keep_arrays: bool = True  # cells layout: keep the plan-order device arrays beside the entries
 
     def __post_init__(self):
         if self.devices < 1 or self.workers_per_device < 1:
@@ -85,8 +91,10 @@ class PlatformConfig:
             raise ValueError("kernel_variant must be 0 (production) or 1 (generic scalar)")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
-        if self.layout not in ("flycoo", "blocked", "panel", "auto"):
-            raise ValueError("layout must be 'flycoo', 'blocked', 'panel' or 'auto'")
+        if self.layout not in ("flycoo", "blocked", "panel", "cells", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked', 'panel', 'cells' or 'auto'")
+        if self.cell_outer_mb < 1 or self.cell_inner_mb < 1:
+            raise ValueError("cell_outer_mb and cell_inner_mb must be >= 1")
 
 
 
@@ -355,6 +363,12 @@ def streamed_blocking(plan, rank, block_mb=32, stream_mb=256):
 def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
     """Put `plan` in the execution layout `cfg.layout` asks for (once)."""
     if cfg.layout == "flycoo" or plan.layout != "flycoo" or cfg.scheduling == "split":
+        return plan
+    if cfg.layout == "cells":
+        prm = choose_cells(plan, rank, cfg, shard_ids)
+        if prm is None:
+            raise ValueError("cells layout needs a 3-mode tensor, R in {16,32,64} and consecutive shards")
+        plan.to_cells(_cell_shards(plan, shard_ids), prm, keep_arrays=cfg.cell_keep_arrays)
         return plan
     if cfg.layout == "panel":
         prm = choose_panels(plan, rank, cfg, shard_ids)
@@ -788,10 +802,148 @@ def choose_panels(plan, rank, cfg: PlatformConfig, shard_ids=None):
     return (slab_shift, shifts, warps)
 
 
+def cell_shape(rank: int, variant: int = 1):
+    """(warps per CTA, steps per pipeline stage, largest stripe rows) of a
+    cells kernel variant, or None."""
+    w = ctypes.c_int32()
+    b = ctypes.c_int32()
+    m = ctypes.c_int32()
+    rc = _lib.lib().skrp_cell_shape(rank, variant, ctypes.byref(w), ctypes.byref(b), ctypes.byref(m))
+    if rc != _lib.SKRP_OK:
+        return None
+    return int(w.value), int(b.value), int(m.value)
+
+
+def _cell_shards(plan, shard_ids):
+    return list(range(plan.shard_count)) if shard_ids is None else sorted(int(j) for j in shard_ids)
+
+
+def choose_cells(plan, rank, cfg: PlatformConfig, shard_ids=None, sms=None):
+    """Parameters of the cells layout (plan.to_cells) or None.
+
+    Outer input = the smaller factor (per round the GPU reads it once and the
+    inner factor once per outer block: rounds x (|outer| + outer_blocks x
+    |inner|)), cut into cfg.cell_outer_mb blocks; inner input in
+    cfg.cell_inner_mb blocks (coarsened until <= 1024 cells).  Stripes: the
+    fewest ROUNDS of #SM x 16 stripes whose panels fit shared memory, rows
+    spread evenly over them."""
+    torch = _torch()
+    n, d = len(plan.shape), plan.mode
+    if n != 3:
+        return None
+    variant = cfg.cell_variant
+    shp = cell_shape(rank, variant)
+    if shp is None and variant != 0:
+        variant, shp = 0, cell_shape(rank, 0)  # the tuned variants are built for R = 32
+    if shp is None:
+        return None
+    warps, stage, max_sr = shp
+    ids = _cell_shards(plan, shard_ids)
+    if not ids or ids != list(range(ids[0], ids[-1] + 1)):
+        return None
+    if sms is None:
+        sms = torch.cuda.get_device_properties(plan.vals.device).multi_processor_count
+    lo, hi = int(plan.bounds[ids[0]]), int(plan.bounds[ids[-1] + 1])
+    rows = max(1, hi - lo)
+    per_round = sms * warps * max_sr
+    rounds = -(-rows // per_round)
+    sr = -(-rows // (rounds * sms * warps))
+    ins = [w for w in range(n) if w != d]
+    om, im = sorted(ins, key=lambda w: (plan.shape[w], w))
+    row_b = rank * 4
+
+    def shift_for(mb, extent):
+        rws = max(1, (mb << 20) // row_b)
+        sh = max(0, rws.bit_length() - 1)
+        return min(sh, max(0, (extent - 1).bit_length()))
+
+    so = shift_for(cfg.cell_outer_mb, plan.shape[om])
+    si = shift_for(cfg.cell_inner_mb, plan.shape[im])
+    nout = -(-plan.shape[om] // (1 << so))
+    while nout * -(-plan.shape[im] // (1 << si)) > 1024:
+        si += 1
+    return {"rank": rank, "stripe_rows": sr, "ctas": sms, "outer_mode": om, "inner_mode": im, "outer_shift": so,
+            "inner_shift": si, "variant": variant, "warps": warps, "stage": stage}
+
+
+class _CellExec:
+    """The cells kernel over the shards the layout was built for: one launch
+    per mode; every owned row is written once (no output zeroing); the result
+    does not depend on the placement."""
+
+    writes_all_rows = True
+
+    def __init__(self, plan, shard_ids, cfg: PlatformConfig, rank, gpu):
+        torch = _torch()
+        c = plan.cells
+        if tuple(_cell_shards(plan, shard_ids)) != c["shard_ids"]:
+            raise ValueError("the cells layout was built for another shard set")
+        self.gpu = gpu
+        self.rank = rank
+        self.c = c
+        self.passes = 1
+        self.levels = []
+        self.tile_nnz = 0
+        self.nnz = int(sum(plan.shards[j].nnz for j in shard_ids))
+        if c["rank"] != rank:
+            raise ValueError(f"the cells layout was built for R={c['rank']}, not R={rank}")
+        self.num_tiles = int(c["stripes"]) if self.nnz else 0
+        self.offsets = c["stripe_offsets"].to(gpu)
+        self.entries = c["entries"].to(gpu)
+        panels = -(-c["stripes"] // c["warps"])
+        rounds = -(-panels // c["ctas"]) if panels else 0
+        self.done = torch.zeros(max(1, rounds * c["cells"]), dtype=torch.int32, device=gpu)
+        self.lag = cfg.cell_lag
+
+    @property
+    def launches(self) -> int:
+        return 1 if self.num_tiles else 0
+
+    def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
+        if self.num_tiles == 0:
+            return
+        c = self.c
+        a = _lib.MttkrpArgs()
+        a.nmodes = len(factors)
+        a.mode = mode
+        a.rank = self.rank
+        a.accumulation = _lib.ACC_DETERMINISTIC
+        a.nnz = nnz_total
+        for w in range(len(factors)):
+            a.factors[w] = None if w == mode else factors[w].data_ptr()
+        a.values = None
+        a.out = out.data_ptr()
+        ca = _lib.CellArgs()
+        ca.row_lo = c["row_lo"]
+        ca.rows = c["rows"]
+        ca.out_row_base = 0
+        ca.stripe_offsets = self.offsets.data_ptr()
+        ca.stripes = c["stripes"]
+        ca.stripe_rows = c["stripe_rows"]
+        ca.ctas = c["ctas"]
+        ca.outer_mode = c["outer_mode"]
+        ca.inner_mode = c["inner_mode"]
+        ca.outer_shift = c["outer_shift"]
+        ca.inner_shift = c["inner_shift"]
+        ca.inner_blocks = c["inner_blocks"]
+        ca.cells = c["cells"]
+        ca.lag = self.lag
+        ca.variant = c["variant"]
+        ca.done = self.done.data_ptr()
+        ca.entries = self.entries.data_ptr()
+        if events is not None:
+            events[0].record()
+        _lib.check(_lib.lib().skrp_mttkrp_cells(ctypes.byref(a), ctypes.byref(ca), stream), "skrp_mttkrp_cells")
+        if events is not None:
+            events[1].record()
+
+
 def _plan_arrays(plan: ModePartitionPlan, gpu):
     """The plan's sorted arrays on `gpu` (copied once and cached if the plan
     was built on another GPU); host-resident (out-of-core) plans are returned
     as they are -- their executor streams them."""
+    if plan.layout == "cells" and plan.vals is None:
+        return None, None  # the cells executor reads the layout's entries
     if plan.vals is None:
         raise ValueError("plan has no device arrays (released)")
     if plan.layout == "host":
@@ -806,6 +958,7 @@ def _plan_arrays(plan: ModePartitionPlan, gpu):
 
 def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
     key = ("exec", tuple(shard_ids), cfg.tile_nnz, cfg.carry_chunk, cfg.accumulation, rank, str(gpu), plan.layout,
+           cfg.cell_lag,
            clip)
     ex = plan._exec_cache.get(key)
     if ex is None:
@@ -813,6 +966,10 @@ def _shard_exec(plan, shard_ids, cfg, rank, gpu, clip=None):
             if clip is not None:
                 raise ValueError("element-split placement needs the plan-order (flycoo) layout")
             ex = _PanelExec(plan, shard_ids, cfg, rank, gpu)
+        elif plan.layout == "cells":
+            if clip is not None:
+                raise ValueError("element-split placement needs the plan-order (flycoo) layout")
+            ex = _CellExec(plan, shard_ids, cfg, rank, gpu)
         elif plan.layout == "host":
             if clip is not None:
                 raise ValueError("element-split placement is not streamed")

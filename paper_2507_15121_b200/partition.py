@@ -34,6 +34,7 @@ from . import _lib
 from .tensor import INDEX_DTYPE, SparseTensorCOO
 
 PLAN_MAGIC = b"SKRPPLN\x00"
+CELL_TAIL_STAGES = 8  # skip entries after the last stripe (csrc/mttkrp_cells.cu CELL_TAIL_STAGES)
 PLAN_VERSION = 1
 STRATEGIES = ("equal-index", "nnz-balanced")
 
@@ -146,6 +147,7 @@ class ModePartitionPlan:
         self.block_order = None
         self.groups = None
         self.panel = None
+        self.cells = None
         self.shards = [
             TensorShard(self, mode, j, (int(self.bounds[j]), int(self.bounds[j + 1])),
                         int(self.offsets[j]), int(self.offsets[j + 1]),
@@ -213,6 +215,8 @@ class ModePartitionPlan:
                 self._host_idx = src._indices[self.order()]
             else:
                 import torch
+                if self.coords is None:
+                    raise ValueError("cells plan: host views need the source tensor and the permutation")
                 arr = torch.stack(self.coords, 1).cpu().numpy().astype(INDEX_DTYPE)
                 self._host_idx = self._to_plan_order(arr)
             self._host_idx.setflags(write=False)
@@ -227,14 +231,18 @@ class ModePartitionPlan:
             if src is not None and src._values is not None and self.perm is not None:
                 self._host_vals = src._values[self.order()]
             else:
+                if self.vals is None:
+                    raise ValueError("cells plan: host views need the source tensor and the permutation")
                 self._host_vals = self._to_plan_order(self.vals.cpu().numpy())
             self._host_vals.setflags(write=False)
         return self._host_vals
 
     def _to_plan_order(self, arr):
-        if self.layout in ("flycoo", "host"):
+        if self.layout in ("flycoo", "host", "cells"):  # cells: the plan-order arrays are untouched
             return arr
         if getattr(self, "exec_perm", None) is None:
+            if self.layout == "cells":
+                raise ValueError("cells plan: host views need the source tensor and the permutation")
             raise ValueError("blocked plan built without its permutation: host views unavailable")
         out = np.empty_like(arr)
         out[self.exec_perm.cpu().numpy().astype(np.int64)] = arr
@@ -410,6 +418,117 @@ class ModePartitionPlan:
         torch.cuda.current_stream(dev).synchronize()
         return self
 
+    def to_cells(self, shard_ids, params, keep_arrays=True):
+        """Build the CELLS execution layout of the GPU-synchronous 2-D blocked
+        kernel (csrc/mttkrp_cells.cu) for the shards `shard_ids` (consecutive:
+        one output row range and one element range).
+
+        A stable GPU sort by [stripe | cell] (stripe = the rows one warp owns;
+        cell = the snake-ordered (outer block, inner block) pair) makes every
+        (stripe, cell) SEGMENT contiguous with rows ascending; every run of
+        one row inside a segment goes whole to the least-loaded slot of the
+        warp (skrp_cell_assign), and the nonzeros are written as 16-byte
+        entries {cell | panel row offset, outer index, inner index, value},
+        each segment's slots interleaved and padded to equal length with skip
+        entries of that cell, so all slots of a warp cross every cell boundary
+        in the same step.  ``params``: dict with rank, stripe_rows, ctas,
+        outer_mode, inner_mode, outer_shift, inner_shift, variant, warps, stage
+        (engine.choose_cells).
+        ``keep_arrays=False`` frees the plan-order device arrays (the entries
+        replace them; host views then need the source tensor + permutation)."""
+        import torch
+
+        if self.layout != "flycoo":
+            raise ValueError("plan is already in a reordered layout")
+        if len(self.shape) != 3:
+            raise ValueError("the cells layout covers 3-mode tensors")
+        ids = sorted(int(j) for j in shard_ids)
+        if not ids or ids != list(range(ids[0], ids[-1] + 1)):
+            raise ValueError("the cells layout needs a run of consecutive shards")
+        d = self.mode
+        lo, hi = int(self.bounds[ids[0]]), int(self.bounds[ids[-1] + 1])
+        e0, e1 = int(self.offsets[ids[0]]), int(self.offsets[ids[-1] + 1])
+        n = e1 - e0
+        p = dict(params)
+        rank = int(p["rank"])
+        if rank not in (16, 32, 64):
+            raise ValueError("the cells layout needs R in {16, 32, 64}")
+        slots = 128 // rank
+        sr, om, im = int(p["stripe_rows"]), int(p["outer_mode"]), int(p["inner_mode"])
+        so, si = int(p["outer_shift"]), int(p["inner_shift"])
+        nout = -(-self.shape[om] // (1 << so))
+        nin = -(-self.shape[im] // (1 << si))
+        cells = nout * nin
+        rows = hi - lo
+        stripes = -(-rows // sr) if rows > 0 else 0
+        nseg = stripes * cells
+        stripe_bits = _key_bits(max(stripes, 1))
+        cell_bits = _key_bits(cells)
+        if cells > 1024 or stripe_bits + cell_bits > 31 or sr * rank * 4 >= (1 << 20):
+            raise ValueError(f"cells layout key too wide ({stripes} stripes, {cells} cells)")
+        dev = self.vals.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rowc, co, ci = self.coords[d], self.coords[om], self.coords[im]
+        seg_len = torch.zeros(max(nseg, 1), dtype=torch.int32, device=dev)
+        sk = perm = slot_t = None
+        if n > 0:
+            keys = torch.empty(n, dtype=torch.int32, device=dev)
+            _lib.call("skrp_cell_keys", rowc[e0:].data_ptr(), co[e0:].data_ptr(), ci[e0:].data_ptr(), n, lo, sr, so,
+                      si, nin, cell_bits, keys.data_ptr(), stream)
+            sk = torch.empty_like(keys)
+            perm = torch.empty_like(keys)
+            bits = stripe_bits + cell_bits
+            ws_bytes = _lib.lib().skrp_sort_workspace_bytes(n, bits)
+            ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+            _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), n, bits, sk.data_ptr(), perm.data_ptr(),
+                      ws.data_ptr(), ws_bytes, stream)
+            del ws
+            rows_sorted = keys  # reuse
+            _lib.call("skrp_gather_u32", rowc[e0:].data_ptr(), perm.data_ptr(), n, rows_sorted.data_ptr(), stream)
+            g = torch.arange(nseg + 1, dtype=torch.int64, device=dev)
+            q = ((g // cells) << cell_bits) + g % cells
+            q[-1] = (1 << 31) - 1
+            seg_off = torch.searchsorted(sk, q.to(torch.int32)).to(torch.int64)
+            seg_off[-1] = n
+            del g, q
+            slot_t = torch.empty(n, dtype=torch.int32, device=dev)
+            _lib.call("skrp_cell_assign", seg_off.data_ptr(), nseg, rows_sorted.data_ptr(), slots, slot_t.data_ptr(),
+                      seg_len.data_ptr(), stream)
+            del rows_sorted, keys, seg_off
+        # segment g of stripe s: [seg_base[g], + slots*seg_len[g]); every stripe
+        # rounded up to whole pipeline stages (params["stage"] steps); skip
+        # entries at the end of the array (the kernel reads ahead)
+        seg_n = seg_len[:nseg].to(torch.int64).reshape(stripes, cells) * slots
+        tot = seg_n.sum(dim=1)
+        unit = int(p["stage"]) * slots
+        tot = (tot + unit - 1) // unit * unit
+        base = torch.zeros(stripes + 1, dtype=torch.int64, device=dev)
+        if stripes:
+            base[1:] = torch.cumsum(tot, 0)
+        seg_base = (base[:-1, None] + torch.cumsum(seg_n, 1) - seg_n).reshape(-1).contiguous()
+        num = int(base[-1].item())
+        total = num + CELL_TAIL_STAGES * unit
+        entries = torch.empty(total * 4, dtype=torch.int32, device=dev)
+        _lib.call("skrp_cell_entries", _lib.ptr(sk), _lib.ptr(perm), _lib.ptr(slot_t), n, cell_bits, cells,
+                  seg_base.data_ptr(), seg_len.data_ptr(), nseg, slots, rowc[e0:].data_ptr(), co[e0:].data_ptr(),
+                  ci[e0:].data_ptr(), self.vals[e0:].data_ptr(), lo, sr, rank * 4, entries.data_ptr(), total, stream)
+        del sk, perm, slot_t, seg_base, seg_len, seg_n
+        torch.cuda.current_stream(dev).synchronize()
+        p.update({"rank": rank, "row_lo": lo, "rows": rows, "stripes": stripes, "stripe_rows": sr,
+                  "slots": slots, "inner_blocks": nin, "outer_blocks": nout, "cells": cells,
+                  "shard_ids": tuple(ids), "stripe_offsets": base, "entries": entries, "num_entries": num,
+                  "elements": (e0, e1), "pad_entries": num - n})
+        self.cells = p
+        self.groups = None
+        self.layout = "cells"
+        self.block_shifts = None
+        self.exec_perm = None  # host views come from the source tensor + permutation
+        if not keep_arrays:
+            self.coords = None
+            self.vals = None
+        self._exec_cache.clear()
+        return self
+
     def to_host(self, pinned=True):
         """Out-of-core execution (the B200 form of the
         reference's per-mode staging, engine.py:103-105): move the sorted
@@ -458,6 +577,7 @@ class ModePartitionPlan:
 
     def release_device(self):
         self.coords = self.vals = self.perm = None
+        self.cells = None
         self._exec_cache.clear()
 
     def __repr__(self):

@@ -305,6 +305,7 @@ class DistributedMttkrp:
             out = self.mode_output(d, facs, None if kernel_events is None else kernel_events[d],
                                    out=None if outputs is None else outputs[d])
             nvtx.range_pop()
+            self._prefetch_next(d + 1 if d + 1 < len(self.plans) else 0)
             if self.world > 1 and exchange:
                 nvtx.range_push(f"skrp mode {plan.mode} all-gather")
                 if outputs is None and self._fused(d):
@@ -317,6 +318,17 @@ class DistributedMttkrp:
             if chained:
                 facs[plan.mode] = out
         return self.outputs
+
+    def _prefetch_next(self, d):
+        """Out-of-core plans: enqueue mode d's leading chunk copies now, so its
+        partition streaming overlaps the all-gather of the mode just launched
+        (north_star (4)); resident plans have nothing to stream."""
+        if self.compute is not None or getattr(self, "_rank_r", None) is None:
+            return
+        ex = self._execs.get((d, self._rank_r))
+        if ex is not None and hasattr(ex, "prefetch"):
+            coords, vals = _plan_arrays(self.plans[d], self.device)
+            ex.prefetch(coords, vals)
 
     def _fused(self, d) -> bool:
         peers = getattr(self, "_peers", None)

@@ -605,18 +605,43 @@ class _StreamExec:
         self.copy_stream = torch.cuda.Stream(gpu)
         self.ready = [torch.cuda.Event() for _ in self.bufs]
         self.free = [torch.cuda.Event() for _ in self.bufs]
+        self.pending = 0  # leading chunks of the next run already enqueued (prefetch)
         self.counter = torch.zeros(1, dtype=torch.int64, device=gpu)
 
     @property
     def launches(self) -> int:
         return len(self.chunks)
 
+    def _copy_chunk(self, i, coords, vals):
+        """Enqueue chunk i's host->device copy on the copy stream (into buffer
+        i % nb, once the kernel that last read that buffer is done)."""
+        torch = _torch()
+        c0, c1, _ = self.chunks[i]
+        b = i % len(self.bufs)
+        bc, bv = self.bufs[b]
+        n = c1 - c0
+        self.copy_stream.wait_event(self.free[b])  # no-op before the buffer's first use
+        with torch.cuda.stream(self.copy_stream):
+            for w in range(len(coords)):
+                bc[w][:n].copy_(coords[w][c0:c1], non_blocking=True)
+            bv[:n].copy_(vals[c0:c1], non_blocking=True)
+            self.ready[b].record(self.copy_stream)
+
+    def prefetch(self, coords, vals):
+        """Start the next run's leading chunk copies now (the runner calls it
+        right after the previous mode's kernel is enqueued), so this mode's
+        partition streaming overlaps that mode's tail and its factor
+        all-gather instead of starting after them (north_star (4))."""
+        k = min(len(self.bufs), len(self.chunks))
+        for i in range(self.pending, k):
+            self._copy_chunk(i, coords, vals)
+        self.pending = max(self.pending, k)
+
     def run(self, coords, vals, nnz_total, mode, factors, out, cfg: PlatformConfig, stream, events=None):
         torch = _torch()
         if not self.chunks:
             return
         cur = torch.cuda.current_stream(self.gpu)
-        cs = self.copy_stream
         a = _lib.MttkrpArgs()
         a.nmodes = len(coords)
         a.mode = mode
@@ -630,28 +655,22 @@ class _StreamExec:
         a.flags = _lib.FLAG_ADDITIVE
         if events is not None:
             events[0].record()
-        cs.wait_stream(cur)  # buffers may still be read by the previous run
         nb = len(self.bufs)
         for i, (c0, c1, tiles) in enumerate(self.chunks):
             b = i % nb
             bc, bv = self.bufs[b]
-            n = c1 - c0
-            if i >= nb:
-                cs.wait_event(self.free[b])
-            with torch.cuda.stream(cs):
-                for w in range(len(coords)):
-                    bc[w][:n].copy_(coords[w][c0:c1], non_blocking=True)
-                bv[:n].copy_(vals[c0:c1], non_blocking=True)
-                self.ready[b].record(cs)
+            if i >= self.pending:  # not prefetched: copy now (double-buffered)
+                self._copy_chunk(i, coords, vals)
             cur.wait_event(self.ready[b])
             for w in range(len(coords)):
                 a.coords[w] = bc[w].data_ptr()
             a.values = bv.data_ptr()
-            a.nnz = n
+            a.nnz = c1 - c0
             a.tiles = tiles.data_ptr()
             a.num_tiles = tiles.numel() // 2
             _lib.check(_lib.lib().skrp_mttkrp_tiles(ctypes.byref(a), cur.cuda_stream), "skrp_mttkrp_tiles")
             self.free[b].record(cur)
+        self.pending = 0
         if events is not None:
             events[1].record()
 

@@ -751,6 +751,14 @@ def test_out_of_core_streamed_modes(m):
     got = [o.double().cpu().numpy() for o in runner.run(dev_f)]
     for d in range(3):
         assert rel_err(got[d], outs[d]) <= TOL
+    # cross-mode prefetch: the runner enqueued mode 0's leading chunks for the
+    # next step while mode 2 ran; a second and third step consume them
+    ex0 = runner._execs[(0, 32)]
+    assert ex0.pending == min(len(ex0.bufs), len(ex0.chunks)) > 0
+    for _ in range(2):
+        again = [o.double().cpu().numpy() for o in runner.run(dev_f)]
+        for d in range(3):
+            assert rel_err(again[d], outs[d]) <= TOL
     with pytest.raises(ValueError, match="atomic"):
         cfgd = sk.PlatformConfig(devices=m, rank=32, accumulation="deterministic-reduce")
         sk.mttkrp_mode(plans[0], sk.make_devices(fs, cfgd), cfgd)

@@ -376,6 +376,10 @@ __global__ void __launch_bounds__(NW * 32, (NW >= 16 ? 1 : 16 / NW))
                                             4 * c4) = v;
             *src = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        // the peer stores must be visible system-wide before this kernel's
+        // completion is observed by the ranks' completion barrier
+        // (distributed._peer_sync): one release fence per item and thread
+        if (pa.num_peers > 0) __threadfence_system();
         if (lockstep) {
             __syncthreads();
             if (threadIdx.x == 0) atomicAdd(a.work_counter, 1ull);

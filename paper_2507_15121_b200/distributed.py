@@ -273,7 +273,11 @@ class DistributedMttkrp:
 
     def _peer_sync(self):
         """All ranks' pushes of this mode are complete before anyone goes on
-        (stream-ordered under NCCL; host barrier under gloo)."""
+        (stream-ordered under NCCL; host barrier under gloo).  The panel
+        kernel ends every item's write-back with __threadfence_system(), so
+        its NVLink stores are visible before its completion -- which the
+        1-element all-reduce (queued behind the kernel on every rank) orders
+        ahead of the next mode's kernel on every rank."""
         import torch
 
         d_ = _dist()

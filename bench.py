@@ -56,20 +56,20 @@ CONFIGS = {
     "cfg3s": dict(shape=(46, 240_000, 240_000), nnz=1_000_000_000, rank=32, dist="uniform",
                   strategy="equal-index", modes=None, host_gen=False,
                   desc="cfg3 Patents-shaped 46x240Kx240K uniform, R=32, all modes, 1.0B nnz (of 3.6B)"),
-    "cfg4s": dict(shape=(8_200_000, 177_000, 8_100_000), nnz=500_000_000, rank=32, dist="zipf",
+    "cfg4s": dict(acc="deterministic-reduce", shape=(8_200_000, 177_000, 8_100_000), nnz=500_000_000, rank=32, dist="zipf",
                   strategy="nnz-balanced", modes=None, host_gen=False,
                   desc="cfg4 Reddit-shaped 8.2Mx177Kx8.1M Zipf(1.2), R=32, all modes, 0.5B nnz (of 4.7B)"),
     # full multi-GPU configs (distributed plan build; one GPU cannot hold them)
     "cfg3": dict(shape=(46, 240_000, 240_000), nnz=3_600_000_000, rank=32, dist="uniform",
                  strategy="equal-index", modes=None, host_gen=False, dist_build=True, park_plans=True,
                  desc="cfg3 Patents-shaped 46x240Kx240K, 3.6B nnz uniform, R=32, all modes"),
-    "cfg4": dict(shape=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, rank=32, dist="zipf",
+    "cfg4": dict(acc="deterministic-reduce", shape=(8_200_000, 177_000, 8_100_000), nnz=4_700_000_000, rank=32, dist="zipf",
                  strategy="nnz-balanced", modes=None, host_gen=False, dist_build=True,
                  desc="cfg4 Reddit-shaped 8.2Mx177Kx8.1M, 4.7B nnz Zipf(1.2), R=32, all modes"),
-    "cfg5": dict(shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=2_000_000_000, rank=64, dist="zipf",
-                 strategy="nnz-balanced", modes=None, host_gen=False, kind="cpd", dist_build=True,
+    "cfg5": dict(acc="deterministic-reduce", shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=2_000_000_000, rank=64, dist="zipf",
+                 strategy="nnz-balanced", modes=None, host_gen=False, kind="cpd", dist_build=True, park_plans=True,
                  desc="cfg5 4-mode 10Mx1Mx100Kx1K, 2B nnz Zipf(1.2), R=64, one full CPD-ALS iteration"),
-    "cfg5s": dict(shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=200_000_000, rank=64, dist="zipf",
+    "cfg5s": dict(acc="deterministic-reduce", shape=(10_000_000, 1_000_000, 100_000, 1_000), nnz=200_000_000, rank=64, dist="zipf",
                   strategy="nnz-balanced", modes=None, host_gen=False, kind="cpd",
                   desc="cfg5 4-mode 10Mx1Mx100Kx1K Zipf(1.2), R=64, one full CPD-ALS iteration, 0.2B nnz (of 2B)"),
 }
@@ -532,6 +532,8 @@ def run_ours(args, cfg):
                            cell_lag=args.cell_lag, cell_variant=args.cell_variant, cell_outer_mb=args.cell_outer_mb,
                            cell_inner_mb=args.cell_inner_mb, cell_keep_arrays=False)
 
+    from paper_2507_15121_b200.engine import apply_layout
+
     t_setup = time.perf_counter()
     dist_build = world > 1 and (args.dist_build or cfg.get("dist_build", False))
     verify = rank == 0 and not dist_build and not args.no_parity and not args.stream_modes and not args.emulate_world
@@ -570,6 +572,11 @@ def run_ours(args, cfg):
                                                     isp_capacity=pcfg.isp_capacity))
                 del src_c, src_v
                 p_.perm = None
+            if park:
+                # the execution layout now, beside the source: with every plan
+                # back in HBM there is no room for its sort temporaries
+                apply_layout(p_, pl, R, list(range(p_.shard_count)))
+                torch.cuda.empty_cache()
             if park and d != modes[-1]:
                 p_.to_host(pinned=False)
             torch.cuda.empty_cache()
@@ -578,10 +585,13 @@ def run_ours(args, cfg):
             # the sampled rows' source nonzeros go to the host now, so the source
             # can leave HBM before the run (phase 2 after the run)
             src_c, src_v = tensor.device_arrays()
-            samples = extract_row_samples(src_c, src_v, shape, modes, rows_per_mode=args.parity_rows)
+            samples = extract_row_samples(src_c, src_v, shape, modes,
+                                          rows_per_mode=args.parity_rows // (4 if cfg.get("kind") == "cpd" else 1))
             del src_c, src_v
-        if cfg.get("kind") != "cpd" or not verify:
-            tensor.drop_device()  # (CP-ALS parity reads the source during its checked iteration)
+        if cfg.get("kind") != "cpd" or not verify or park:
+            # (CP-ALS parity reads the source during its checked iteration,
+            # unless the plans need its HBM: then the extracted rows serve)
+            tensor.drop_device()
         torch.cuda.empty_cache()
         for p_ in plans:
             if p_.layout == "host":
@@ -608,8 +618,10 @@ def run_ours(args, cfg):
     runner.prepare(R)
     setup_s = time.perf_counter() - t_setup
     if cfg.get("kind") == "cpd":
+        park_cpd = world == 1 and cfg.get("park_plans", False)
         return run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s,
-                       tensor=tensor if verify else None, plan_checks=plan_checks)
+                       tensor=tensor if verify and not park_cpd else None, plan_checks=plan_checks,
+                       samples=samples if verify and park_cpd else None)
 
     for _ in range(args.warmup):
         runner.run(dev_f)
@@ -861,7 +873,7 @@ def emulate_world(args, cfg, plans, pl, dev_f, dev, build_s, link_gbs=775.0):
 
 
 def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_s, build_s, tensor=None,
-            plan_checks=()):
+            plan_checks=(), samples=None):
     """cfg5: one full CPD-ALS iteration per step (all modes: MTTKRP, solve,
     normalisation, factor all-gather, Grams, fit)."""
     import torch
@@ -909,16 +921,22 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
     roof = roofline_block(args.config, list(range(nm)), runner, dev_f, kern, alg, comp, peak, peak_src, world)
     roof["mttkrp_share_of_iteration"] = sum(kern) / step_s
     parity = None
-    if tensor is not None:
+    if tensor is not None or samples is not None:
         # one more iteration with the checker hooked into every mode update:
         # sampled MTTKRP rows and the ALS update M V^-1 of those rows, in fp64
         # from the source tensor (oracle/scale.py cpd_mode_check)
-        from oracle.scale import cpd_mode_check
+        from oracle.scale import cpd_mode_check, cpd_mode_check_extracted
 
-        src_c, src_v = tensor.device_arrays()
         checks = []
-        als.run(dev_f, iterations=1, observe=lambda d, facs, m, new, lam: checks.append(
-            cpd_mode_check(src_c, src_v, cfg["shape"], d, facs, m, new, lam, rows_per_mode=args.parity_rows // 4)))
+        if tensor is not None:
+            src_c, src_v = tensor.device_arrays()
+            als.run(dev_f, iterations=1, observe=lambda d, facs, m, new, lam: checks.append(
+                cpd_mode_check(src_c, src_v, cfg["shape"], d, facs, m, new, lam,
+                               rows_per_mode=args.parity_rows // 4)))
+        else:  # full size on one GPU: rows extracted before the source left HBM
+            by_mode = {smp["mode"]: smp for smp in samples}
+            als.run(dev_f, iterations=1, observe=lambda d, facs, m, new, lam: checks.append(
+                cpd_mode_check_extracted(by_mode[d], cfg["shape"], d, facs, m, new, lam)))
         worst = max(max(c["max_rel_err_mttkrp"], c["max_rel_err_update"]) for c in checks)
         parity = {"rows_checked": sum(c["rows"] for c in checks), "max_rel_err": worst, "tolerance": 1e-4,
                   "ok": worst <= 1e-4, "per_mode": checks, "plans": list(plan_checks),
@@ -927,7 +945,8 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
                             "from the SOURCE tensor vs the GPU's M; the ALS update of those rows (M V^-1, V = "
                             "Hadamard of fp64 Grams of the factors the GPU used, applied to the GPU's M) vs the "
                             "GPU's new*lambda (oracle/scale.py cpd_mode_check)"}
-        tensor.drop_device()
+        if tensor is not None:
+            tensor.drop_device()
     if rank == 0:
         line = {
             "metric": METRIC, "value": nm * cfg["nnz"] / step_s, "unit": "nnz/s", "n_gpus": world,
@@ -1042,7 +1061,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--accumulation", default="atomic", choices=("deterministic-reduce", "atomic"))
+    ap.add_argument("--accumulation", default=None, choices=("deterministic-reduce", "atomic"),
+                    help="default: the config's (atomic for uniform rows; deterministic-reduce for the Zipf configs, "
+                         "whose head rows sum 10^8 nonzeros: the fp64 carry tree keeps them within 1e-4)")
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = auto)")
     ap.add_argument("--layout", default="auto", choices=("flycoo", "blocked", "panel", "cells", "auto"))
     ap.add_argument("--cell-lag", type=int, default=0, help="cells layout: lag in cells (0 = free running)")
@@ -1082,6 +1103,8 @@ def main():
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         print("note: warmup < 3 is below the timing rules; proceeding", file=sys.stderr)
     cfg = CONFIGS[args.config]
+    if args.accumulation is None:
+        args.accumulation = cfg.get("acc", "atomic")
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

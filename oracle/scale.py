@@ -227,6 +227,17 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
             if w != d:
                 contrib *= f64[w].index_select(0, _u32(src_coords[w].index_select(0, s_)))
         expect.index_add_(0, torch.searchsorted(rows_t, _u32(col.index_select(0, s_))), contrib)
+    return _cpd_update_check(rows_t, expect, tot, shape, d, f64, m, new, lambdas)
+
+
+def _cpd_update_check(rows_t, expect, tot, shape, d, f64, m, new, lambdas):
+    """The MTTKRP and ALS-update comparisons of cpd_mode_check for the sampled
+    rows `rows_t` with their fp64 MTTKRP `expect` (f64: the factors the GPU
+    used, in fp64)."""
+    import torch
+
+    dev = m.device
+    R = m.shape[1]
     got_m = m.index_select(0, rows_t).double()
     err_m = float(((got_m - expect).abs() / expect.abs().clamp(min=1.0)).max().item())
     v = torch.ones((R, R), dtype=torch.float64, device=dev)
@@ -251,3 +262,27 @@ def cpd_mode_check(src_coords, src_vals, shape, d, facs, m, new, lambdas, rows_p
     return {"mode": d, "rows": int(rows_t.numel()), "nnz": tot, "max_rel_err_mttkrp": err_m,
             "max_rel_err_update": err_u, "max_rel_err_update_vs_fp64_source": err_e2e,
             "cond_V": float(torch.linalg.cond(v).item())}
+
+
+def cpd_mode_check_extracted(sample, shape, d, facs, m, new, lambdas):
+    """cpd_mode_check from rows extracted before the source left HBM
+    (extract_row_samples: full-size cfg5 on one GPU): the sampled rows'
+    MTTKRP in fp64 from their SOURCE nonzeros with the factors the GPU used,
+    then the same MTTKRP and update comparisons."""
+    import torch
+
+    dev = m.device
+    R = m.shape[1]
+    f64 = [f.double() for f in facs]
+    rows_t = torch.from_numpy(sample["rows"]).to(dev)
+    expect = torch.zeros((rows_t.numel(), R), dtype=torch.float64, device=dev)
+    nsel = sample["coords"].shape[0]
+    for a in range(0, nsel, 1 << 22):
+        coords = torch.from_numpy(sample["coords"][a:a + (1 << 22)]).to(dev)
+        contrib = torch.from_numpy(sample["vals"][a:a + (1 << 22)]).to(dev)[:, None].expand(-1, R).clone()
+        for w in range(coords.shape[1]):
+            if w != d:
+                contrib *= f64[w].index_select(0, coords[:, w])
+        expect.index_add_(0, torch.searchsorted(rows_t, coords[:, d].contiguous()), contrib)
+        del coords, contrib
+    return _cpd_update_check(rows_t, expect, int(nsel), shape, d, f64, m, new, lambdas)

@@ -536,11 +536,15 @@ class ModePartitionPlan:
         (engine._StreamExec) copies them back chunk by chunk, overlapped with
         the kernel, every time the mode runs.  Plan order only.
         ``pinned=False`` parks the arrays in pageable memory of their exact
-        size (a build parking finished plans; see to_device)."""
+        size (a build parking finished plans; see to_device) -- in any
+        execution layout except cells, which to_device restores."""
         import torch
 
-        if self.layout != "flycoo":
+        if pinned and self.layout != "flycoo":
             raise ValueError("out-of-core execution streams the plan (FLYCOO) order")
+        if self.layout in ("host", "cells"):
+            raise ValueError(f"cannot park a plan in the {self.layout!r} layout")
+        self._parked_layout = self.layout if not pinned else "flycoo"
 
         def pin(t):
             if not pinned:
@@ -553,6 +557,8 @@ class ModePartitionPlan:
         self.vals = pin(self.vals)
         if self.perm is not None:
             self.perm = self.perm.cpu()
+        if getattr(self, "exec_perm", None) is not None:
+            self.exec_perm = self.exec_perm.cpu()
         self.layout = "host"
         self._exec_cache.clear()
         return self
@@ -570,8 +576,10 @@ class ModePartitionPlan:
         self.vals = self.vals.to(dev, non_blocking=True)
         if self.perm is not None:
             self.perm = self.perm.to(dev)
+        if getattr(self, "exec_perm", None) is not None and not self.exec_perm.is_cuda:
+            self.exec_perm = self.exec_perm.to(dev)
         torch.cuda.current_stream(dev).synchronize()
-        self.layout = "flycoo"
+        self.layout = getattr(self, "_parked_layout", "flycoo")
         self._exec_cache.clear()
         return self
 

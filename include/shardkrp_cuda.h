@@ -72,6 +72,10 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
                                     loaded L2::evict_first so they do not push
                                     the pinned block out (R = 32, N = 3) */
 #define SKRP_FLAG_STREAM_INPUT1 4 /* same for input 1 */
+#define SKRP_FLAG_FIBER_INPUT0 16 /* FIBER layout (R = 32, N = 3): inside every shard the nonzeros
+                                    are sorted by (c_d, c_f) with f = input 0 (the first mode != mode):
+                                    a run of one (row, fiber) gathers input f's row once */
+#define SKRP_FLAG_FIBER_INPUT1 32 /* same with f = input 1 */
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);

@@ -23,6 +23,8 @@ ACC_DETERMINISTIC, ACC_ATOMIC = 0, 1
 FLAG_ADDITIVE = 1
 FLAG_STREAM_INPUT0 = 2
 FLAG_STREAM_INPUT1 = 4
+FLAG_FIBER_INPUT0 = 16
+FLAG_FIBER_INPUT1 = 32
 PANEL_LOCKSTEP = 1
 
 vp = ctypes.c_void_p

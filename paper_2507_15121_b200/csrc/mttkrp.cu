@@ -417,6 +417,9 @@ static Variant choose(const skrp_mttkrp_args &a)
             const int sm = a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1);
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 64 | 2, 1>();
             if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 64 | 4, 1>();
+            // fiber layout: the fiber input's row is gathered once per (row, fiber) run
+            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<3, 4, 4, 2, 64 | 512, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<3, 4, 4, 2, 64 | 512 | 1024, 1>();
             return mk2<3, 4, 4, 2, 64, 1>();
         }
         if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;

@@ -68,7 +68,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     constexpr int CPL = (RR + 31) / 32;  // columns per lane in the column layout
     constexpr int STREAMED = PLAIN & 6;
     constexpr bool SPLITFMA = (PLAIN & 64) != 0;
+    // PLAIN bit 512: FIBER reuse (fiber layout: nonzeros sorted by (row, c_f)
+    // inside every shard, f = input JF = bit 1024 ? 1 : 0).  A batch whose 32
+    // nonzeros share the running row AND fiber gathers only the other input:
+    // t += v * C[k] per slot; the fiber's row F[f] is gathered once when the
+    // fiber ends (acc += t * F[f]) -- half the gathered bytes on long fibers
+    constexpr bool FIB = (PLAIN & 512) != 0;
+    constexpr int JF = (PLAIN & 1024) ? 1 : 0;
+    constexpr int JO = 1 - JF;
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
+    static_assert(!FIB || (G == 32 && NIN == 2 && STREAMED == 0), "fiber reuse: 3 modes, one group per batch");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -126,6 +135,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         float acc[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+        // FIB: the open fiber (coordinate curf of input JF) and its partial sum
+        uint32_t curf = 0xffffffffu;
+        bool tpend = false;
+        float tacc[FIB ? VEC : 1];
+#pragma unroll
+        for (int i = 0; i < (FIB ? VEC : 1); ++i) tacc[i] = 0.f;
+        auto fold_fiber = [&]() {  // acc += t * F_JF[curf], per slot (linear in the slots)
+            if constexpr (FIB) {
+                if (tpend) {
+                    float bf[VEC];
+                    ld_row<VEC>(bf, frow(JF, curf), pol_row);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        acc[i] = fmaf(tacc[i], bf[i], acc[i]);
+                        tacc[i] = 0.f;
+                    }
+                    tpend = false;
+                }
+            }
+        };
 
         auto reduce_slots = [&]() {
 #pragma unroll
@@ -245,6 +274,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
             advance(base);
             const bool uniform = __all_sync(kFull, r_l == cur);
+            if constexpr (FIB) {
+                if (__all_sync(kFull, r_l == cur && c_l[JF] == curf)) {
+                    // one row, one fiber: only the other input is gathered
+                    float go[U][VEC];
+                    float vv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = slot * U + u;
+                        vv[u] = __shfl_sync(kFull, v_l, e);
+                        ld_row<VEC>(go[u], frow(JO, __shfl_sync(kFull, c_l[JO], e)), pol_row);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) tacc[i] = fmaf(vv[u], go[u][i], tacc[i]);
+                    tpend = true;
+                    continue;
+                }
+                fold_fiber();
+                curf = __shfl_sync(kFull, c_l[JF], nin - 1);
+            }
 
             // Batch classes: 0 = every row is `cur` (registers only);
             // 1 = exactly one row boundary at e_b (two register accumulators);
@@ -439,6 +489,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             for (int i = 0; i < VEC; ++i) acc[i] = (slot == 0) ? carry_row[col + i] : 0.f;
             __syncwarp();
         }
+        fold_fiber();
         if constexpr (TRED && VEC >= S) {
             write_tred(cur, head, true);
         } else {

@@ -71,6 +71,7 @@ class PlatformConfig:
     panel_lockstep: bool = True  # panel layout: items in grid-synchronised rounds (uniform item sizes)
     stream_chunk_nnz: int = 1 << 27  # out-of-core plans: nonzeros per streamed chunk (2 device buffers)
     fused_allgather: bool = False  # N>1, panel layout: push finished rows into peers' outputs (CUDA IPC)
+    fibers: bool = True         # auto layout: the fiber layout where (row, c_f) runs are long (3 modes, R = 32)
     cell_outer_mb: int = 32     # cells layout: outer input block (MB of factor rows)
     cell_inner_mb: int = 8      # cells layout: inner input block
     cell_lag: int = 0           # cells layout: cells a warp may run ahead of the slowest CTA (0 = free running:
@@ -91,8 +92,8 @@ class PlatformConfig:
             raise ValueError("kernel_variant must be 0 (production) or 1 (generic scalar)")
         if self.tile_nnz < 0 or self.carry_chunk < 2:
             raise ValueError("tile_nnz must be >= 0 (0 = auto) and carry_chunk >= 2")
-        if self.layout not in ("flycoo", "blocked", "panel", "cells", "auto"):
-            raise ValueError("layout must be 'flycoo', 'blocked', 'panel', 'cells' or 'auto'")
+        if self.layout not in ("flycoo", "blocked", "panel", "cells", "fibers", "auto"):
+            raise ValueError("layout must be 'flycoo', 'blocked', 'panel', 'cells', 'fibers' or 'auto'")
         if self.cell_outer_mb < 1 or self.cell_inner_mb < 1:
             raise ValueError("cell_outer_mb and cell_inner_mb must be >= 1")
 
@@ -376,6 +377,13 @@ def apply_layout(plan, cfg: PlatformConfig, rank: int, shard_ids=None):
             raise ValueError("panel layout needs R in {8,16,32,64} and 3..5 modes")
         plan.to_panels(*prm)
         return plan
+    if cfg.layout == "fibers" or (cfg.layout == "auto" and cfg.fibers and cfg.scheduling != "split"):
+        f = choose_fibers(plan, rank)
+        if f is not None:
+            plan.to_fibers(f)
+            return plan
+        if cfg.layout == "fibers":
+            raise ValueError("fiber layout needs a 3-mode tensor, R = 32 and long (row, c_f) runs")
     if rank not in _V2_RANKS or len(plan.shape) > 5:
         if cfg.layout == "blocked":
             raise ValueError("blocked layout needs R in {8,16,32,64,128} and N <= 5")
@@ -454,7 +462,7 @@ class _ShardExec:
         self.blocked = plan.layout == "blocked"
         if clip is not None and self.blocked:
             raise ValueError("element-split placement needs the plan-order (flycoo) layout")
-        self.flags = (_lib.FLAG_ADDITIVE if self.blocked else 0) | _stream_flags(plan, rank)
+        self.flags = (_lib.FLAG_ADDITIVE if self.blocked else 0) | _stream_flags(plan, rank) | _fiber_flags(plan, rank)
         self.nnz = (int(clip[1] - clip[0]) if clip is not None
                     else int(sum(plan.shards[j].nnz for j in shard_ids)))
         self.tile_nnz = cfg.tile_nnz or auto_tile_nnz(plan_global_nnz(plan), gpu)
@@ -538,6 +546,35 @@ class _ShardExec:
                 rows_in, vals_in, in_f64 = lvl["rows_out"], lvl["vals_out"], 1
         if events is not None:
             events[1].record()
+
+
+def _fiber_flags(plan, rank) -> int:
+    """SKRP_FLAG_FIBER_INPUTj for a plan in the fiber layout (tile kernel,
+    R = 32, 3 modes): j = position of the fiber mode among the inputs."""
+    if plan.layout != "fibers" or len(plan.shape) != 3 or rank != 32:
+        return 0
+    ins = [w for w in range(3) if w != plan.mode]
+    return _lib.FLAG_FIBER_INPUT0 if ins.index(plan.fiber_mode) == 0 else _lib.FLAG_FIBER_INPUT1
+
+
+def choose_fibers(plan, rank, min_fiber=8.0):
+    """Fiber mode for the fiber layout, or None: the input mode with the
+    fewest rows (the longest (row, c_f) runs), if the expected fiber length
+    -- nnz / sum_rows I_f (1 - exp(-n_row / I_f)), the uniform-draw number
+    of distinct (row, c_f) pairs -- is at least `min_fiber` (cfg3: ~325 in
+    every mode; cfg2, cfg4: ~1)."""
+    torch = _torch()
+    n, d = len(plan.shape), plan.mode
+    if n != 3 or rank != 32 or plan.nnz == 0:
+        return None
+    f = min((w for w in range(n) if w != d), key=lambda w: (plan.shape[w], w))
+    rows = plan.coords[d]
+    counts = torch.empty(plan.shape[d], dtype=torch.int64, device=rows.device)
+    _lib.call("skrp_histogram", rows.data_ptr(), rows.numel(), counts.numel(), counts.data_ptr(),
+              torch.cuda.current_stream(rows.device).cuda_stream)
+    i_f = float(plan.shape[f])
+    pairs = float((i_f * (1.0 - torch.exp(-counts.double() / i_f))).sum().item())
+    return f if pairs > 0 and plan.nnz / pairs >= min_fiber else None
 
 
 def _stream_flags(plan, rank) -> int:

@@ -308,42 +308,110 @@ class ModePartitionPlan:
         torch.cuda.current_stream(dev).synchronize()
         return self
 
-    def _reorder_by_key(self, parts, shard_bits):
+    def _reorder_by_key(self, parts, shard_bits, need_keys=True, seg_cap=1 << 29):
         """Stable-sort the device arrays IN PLACE by [shard | parts...] (parts:
         (coordinate array, shift, width) in key order); returns the sorted keys.
         Keeps ``exec_perm`` (device position -> plan position) when the plan
-        keeps its permutation (host views)."""
+        keeps its permutation (host views).  ``need_keys=False``: the keys
+        never reorder across shards, so runs of consecutive shards of at most
+        ``seg_cap`` nonzeros (or one larger shard) are sorted one at a time --
+        temporaries scale with the run, not the plan (full-size cfg3 sorts
+        beside its source tensor) -- and nothing is returned."""
         import torch
 
         nnz = self.nnz
         dev = self.vals.device
         stream = torch.cuda.current_stream(dev).cuda_stream
         total_bits = shard_bits + sum(p[2] for p in parts)
-        starts = torch.from_numpy(np.ascontiguousarray(self.offsets)).to(dev)
-        keys = torch.empty(nnz, dtype=torch.int32, device=dev)
-        cptr = (_lib.vp * len(parts))(*[p[0].data_ptr() for p in parts])
-        sh = np.ascontiguousarray([p[1] for p in parts], dtype=np.int32)
-        wd = np.ascontiguousarray([p[2] for p in parts], dtype=np.int32)
-        _lib.call("skrp_block_keys", cptr, len(parts), sh.ctypes.data, wd.ctypes.data, starts.data_ptr(),
-                  self.shard_count, shard_bits, nnz, keys.data_ptr(), stream)
-        sorted_keys = torch.empty_like(keys)
-        perm = torch.empty_like(keys)
-        ws_bytes = _lib.lib().skrp_sort_workspace_bytes(nnz, total_bits)
-        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
-        _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), nnz, total_bits, sorted_keys.data_ptr(),
-                  perm.data_ptr(), ws.data_ptr(), ws_bytes, stream)
-        del ws, keys
-        for w in range(len(self.shape)):
-            out = torch.empty_like(self.coords[w])
-            _lib.call("skrp_gather_u32", self.coords[w].data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
-            self.coords[w] = out
-        out = torch.empty_like(self.vals)
-        _lib.call("skrp_gather_u32", self.vals.data_ptr(), perm.data_ptr(), nnz, out.data_ptr(), stream)
-        self.vals = out
+        if need_keys or nnz <= seg_cap:
+            segs = [(0, self.shard_count)]
+        else:
+            segs, j0 = [], 0
+            while j0 < self.shard_count:
+                j1 = j0 + 1
+                while j1 < self.shard_count and self.offsets[j1 + 1] - self.offsets[j0] <= seg_cap:
+                    j1 += 1
+                segs.append((j0, j1))
+                j0 = j1
+        keep_perm = self.perm is not None
+        full_perm = torch.empty(nnz, dtype=torch.int32, device=dev) if keep_perm and len(segs) > 1 else None
+        sorted_keys = None
+        for j0, j1 in segs:
+            e0, e1 = int(self.offsets[j0]), int(self.offsets[j1])
+            n = e1 - e0
+            if n == 0:
+                continue
+            starts = torch.from_numpy(np.ascontiguousarray(self.offsets[j0:j1 + 1] - e0)).to(dev)
+            keys = torch.empty(n, dtype=torch.int32, device=dev)
+            cptr = (_lib.vp * len(parts))(*[p[0][e0:].data_ptr() for p in parts])
+            sh = np.ascontiguousarray([p[1] for p in parts], dtype=np.int32)
+            wd = np.ascontiguousarray([p[2] for p in parts], dtype=np.int32)
+            _lib.call("skrp_block_keys", cptr, len(parts), sh.ctypes.data, wd.ctypes.data, starts.data_ptr(),
+                      j1 - j0, shard_bits, n, keys.data_ptr(), stream)
+            sk = torch.empty_like(keys)
+            perm = torch.empty_like(keys)
+            ws_bytes = _lib.lib().skrp_sort_workspace_bytes(n, total_bits)
+            ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+            _lib.call("skrp_stable_sort_by_key", keys.data_ptr(), n, total_bits, sk.data_ptr(), perm.data_ptr(),
+                      ws.data_ptr(), ws_bytes, stream)
+            del ws, keys
+            if not need_keys:
+                del sk
+                sk = None
+            for w in range(len(self.shape)):
+                out = torch.empty(n, dtype=self.coords[w].dtype, device=dev)
+                _lib.call("skrp_gather_u32", self.coords[w][e0:].data_ptr(), perm.data_ptr(), n, out.data_ptr(),
+                          stream)
+                if n == nnz:
+                    self.coords[w] = out
+                else:
+                    self.coords[w][e0:e1].copy_(out)
+                del out
+            out = torch.empty(n, dtype=self.vals.dtype, device=dev)
+            _lib.call("skrp_gather_u32", self.vals[e0:].data_ptr(), perm.data_ptr(), n, out.data_ptr(), stream)
+            if n == nnz:
+                self.vals = out
+            else:
+                self.vals[e0:e1].copy_(out)
+            del out
+            if full_perm is not None:
+                full_perm[e0:e1] = perm + e0
+            elif keep_perm:
+                full_perm = perm  # one segment covering the plan
+            sorted_keys = sk
         # device position i holds plan-order element exec_perm[i] (kept only when
         # the plan keeps its permutation, i.e. host views are wanted)
-        self.exec_perm = perm if self.perm is not None else None
+        self.exec_perm = full_perm if keep_perm else None
         return sorted_keys
+
+    def to_fibers(self, fiber_mode):
+        """Reorder the device arrays IN PLACE into the FIBER execution layout:
+        inside every shard the nonzeros are sorted by (c_d, c_f) (stable), so
+        each run of one row is cut into FIBERS of one c_f -- the tile kernel
+        gathers F_f's row once per fiber instead of once per nonzero (CSF-style
+        reuse; cfg3: ~325 nonzeros per fiber in every mode).  Rows stay
+        contiguous inside shards and tiles; shard offsets and host views
+        (through the permutation) are unchanged.  Sorted shard run by shard
+        run: the temporaries scale with a run, not the plan."""
+        import torch
+
+        if self.layout != "flycoo":
+            raise ValueError("plan is already in a reordered layout")
+        n, d, f = len(self.shape), self.mode, int(fiber_mode)
+        if not (0 <= f < n) or f == d:
+            raise ValueError("fiber_mode must be an input mode")
+        shard_bits = max(1, _key_bits(self.shard_count))
+        rb, fb = max(1, _key_bits(self.shape[d])), max(1, _key_bits(self.shape[f]))
+        if shard_bits + rb + fb > 32:
+            raise ValueError(f"fiber key needs {shard_bits + rb + fb} > 32 bits")
+        self._reorder_by_key([(self.coords[d], 0, rb), (self.coords[f], 0, fb)], shard_bits, need_keys=False)
+        self.layout = "fibers"
+        self.fiber_mode = f
+        self.groups = None
+        self.block_shifts = None
+        self._exec_cache.clear()
+        torch.cuda.current_stream(self.vals.device).synchronize()
+        return self
 
     def to_panels(self, slab_shift, shifts, warps, order=None, sweep=None):
         """Reorder the device arrays IN PLACE into the PANEL execution layout

@@ -1009,3 +1009,35 @@ def test_measure_isolated_compute_per_device_shares():
     # each quarter share runs faster than the whole, and the whole costs no
     # more than its parts (launch overheads make small shares relatively dear)
     assert max(four) < one[0] < 1.5 * sum(four), (four, one)
+
+
+@pytest.mark.parametrize("acc", ["atomic", "deterministic-reduce"])
+def test_fiber_layout_parity(golden, acc):
+    """Fiber layout (plan.to_fibers, picked by layout='auto' where (row, c_f)
+    runs are long -- the cfg3 shape): the tile kernel gathers the fiber
+    input's row once per run; chained all-mode parity with the oracle, host
+    plan views still the reference order, the fiber instantiation ran, and
+    deterministic-reduce stays bit-identical across device counts."""
+    t = sk.synth_tensor((46, 3000, 2500), 2_000_000, seed=17)
+    fs = sk.random_factors(t.shape, 32, seed=8)
+    ref_plans = [p._indices.copy() for p in sk.build_all_plans(t, sk.PartitionConfig(devices=2))]
+    results = []
+    for m in (1, 2):
+        plans = sk.build_all_plans(t, sk.PartitionConfig(devices=2))
+        cfg = sk.PlatformConfig(devices=m, rank=32, accumulation=acc, layout="auto", tile_nnz=1024)
+        _lib.launch_log(clear=True)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        assert all(p.layout == "fibers" for p in plans), [p.layout for p in plans]
+        names = [n for _, n in _lib.launch_log()]
+        assert any("576" in n or "1600" in n for n in names), names
+        for p, before in zip(plans, ref_plans):
+            assert np.array_equal(p._indices, before)
+        results.append(outs)
+    facs = [f.data.copy() for f in fs]
+    for d in range(3):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+        assert rel_err(results[0][d], expect) <= TOL
+        facs[d] = results[0][d]
+    if acc == "deterministic-reduce":
+        for a, b in zip(results[0], results[1]):
+            assert np.array_equal(a, b)

@@ -384,7 +384,7 @@ class ModePartitionPlan:
         self.exec_perm = full_perm if keep_perm else None
         return sorted_keys
 
-    def to_fibers(self, fiber_mode):
+    def to_fibers(self, fiber_mode, seg_cap=1 << 29):
         """Reorder the device arrays IN PLACE into the FIBER execution layout:
         inside every shard the nonzeros are sorted by (c_d, c_f) (stable), so
         each run of one row is cut into FIBERS of one c_f -- the tile kernel
@@ -404,7 +404,8 @@ class ModePartitionPlan:
         rb, fb = max(1, _key_bits(self.shape[d])), max(1, _key_bits(self.shape[f]))
         if shard_bits + rb + fb > 32:
             raise ValueError(f"fiber key needs {shard_bits + rb + fb} > 32 bits")
-        self._reorder_by_key([(self.coords[d], 0, rb), (self.coords[f], 0, fb)], shard_bits, need_keys=False)
+        self._reorder_by_key([(self.coords[d], 0, rb), (self.coords[f], 0, fb)], shard_bits, need_keys=False,
+                             seg_cap=seg_cap)
         self.layout = "fibers"
         self.fiber_mode = f
         self.groups = None

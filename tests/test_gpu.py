@@ -1041,3 +1041,27 @@ def test_fiber_layout_parity(golden, acc):
     if acc == "deterministic-reduce":
         for a, b in zip(results[0], results[1]):
             assert np.array_equal(a, b)
+
+
+def test_fiber_reorder_segmented_matches_whole():
+    """to_fibers sorts shard run by shard run (seg_cap): the device arrays and
+    the execution permutation are identical to one whole-plan sort, the
+    arrays are (c_d, c_f)-sorted inside every shard and the shards keep their
+    nonzeros; empty shards are fine."""
+    t = sk.synth_tensor((40, 900, 700), 300_000, seed=23)
+    a = sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=8))  # 32 shards requested, clamped to 40 rows
+    b = sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=8))
+    a.to_fibers(2)
+    b.to_fibers(2, seg_cap=10_000)  # many runs of consecutive shards
+    for x, y in zip(a.coords + [a.vals], b.coords + [b.vals]):
+        assert torch.equal(x, y)
+    assert torch.equal(a.exec_perm, b.exec_perm)
+    rows = b.coords[0].cpu().numpy().astype(np.int64)
+    fib = b.coords[2].cpu().numpy().astype(np.int64)
+    key = rows * 1000 + fib
+    for s_ in b.shards:
+        seg = key[s_.start:s_.stop]
+        assert np.all(np.diff(seg) >= 0)
+        lo, hi = s_.index_range
+        assert np.all((rows[s_.start:s_.stop] >= lo) & (rows[s_.start:s_.stop] < hi))
+    assert np.array_equal(b._indices, sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=8))._indices)

@@ -76,6 +76,8 @@ typedef struct CUstream_st *skrp_stream_t; /* == cudaStream_t */
                                     are sorted by (c_d, c_f) with f = input 0 (the first mode != mode):
                                     a run of one (row, fiber) gathers input f's row once */
 #define SKRP_FLAG_FIBER_INPUT1 32 /* same with f = input 1 */
+#define SKRP_FLAG_FIBER_INPUT2 64 /* same with f = input 2 (4-mode, R = 64) */
+#define SKRP_FLAG_FIBER_MASK (SKRP_FLAG_FIBER_INPUT0 | SKRP_FLAG_FIBER_INPUT1 | SKRP_FLAG_FIBER_INPUT2)
 
 /* ----------------------------------------------------------------- misc */
 int skrp_last_error(char *buf, size_t len);

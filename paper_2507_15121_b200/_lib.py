@@ -25,6 +25,7 @@ FLAG_STREAM_INPUT0 = 2
 FLAG_STREAM_INPUT1 = 4
 FLAG_FIBER_INPUT0 = 16
 FLAG_FIBER_INPUT1 = 32
+FLAG_FIBER_INPUT2 = 64
 PANEL_LOCKSTEP = 1
 
 vp = ctypes.c_void_p

@@ -420,6 +420,16 @@ static Variant choose(const skrp_mttkrp_args &a)
             // fiber layout: the fiber input's row is gathered once per (row, fiber) run
             if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<3, 4, 4, 2, 64 | 512, 1>();
             if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<3, 4, 4, 2, 64 | 512 | 1024, 1>();
+        }
+        if (a.nmodes == 4 && a.rank == 64 && (a.flags & SKRP_FLAG_FIBER_MASK) &&
+            !(a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1))) {
+            // 4-mode fiber layout (cfg5): two gathered inputs per nonzero, the
+            // fiber input's row once per run
+            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<4, 8, 2, 2, 512, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<4, 8, 2, 2, 512 | 1024, 1>();
+            return mk2<4, 8, 2, 2, 512 | 2048, 1>();
+        }
+        if (a.nmodes == 3 && a.rank == 32) {
             return mk2<3, 4, 4, 2, 64, 1>();
         }
         if (a.nmodes == 3 && pick_v2<3>(a.rank, v)) return v;

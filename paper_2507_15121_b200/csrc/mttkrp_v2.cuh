@@ -74,10 +74,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     // t += v * C[k] per slot; the fiber's row F[f] is gathered once when the
     // fiber ends (acc += t * F[f]) -- half the gathered bytes on long fibers
     constexpr bool FIB = (PLAIN & 512) != 0;
-    constexpr int JF = (PLAIN & 1024) ? 1 : 0;
-    constexpr int JO = 1 - JF;
+    constexpr int JF = (PLAIN >> 10) & 3;  // bits 1024 / 2048: the fiber input
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
-    static_assert(!FIB || (G == 32 && NIN == 2 && STREAMED == 0), "fiber reuse: 3 modes, one group per batch");
+    static_assert(!FIB || (STREAMED == 0 && JF < NIN), "fiber reuse: no streamed input");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -276,19 +275,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             const bool uniform = __all_sync(kFull, r_l == cur);
             if constexpr (FIB) {
                 if (__all_sync(kFull, r_l == cur && c_l[JF] == curf)) {
-                    // one row, one fiber: only the other input is gathered
-                    float go[U][VEC];
-                    float vv[U];
+                    // one row, one fiber: only the other inputs are gathered
+                    constexpr int NO = NIN - 1;
+#pragma unroll 1
+                    for (int g0 = 0; g0 < 32; g0 += G) {
+                        float go[U][NO][VEC];
+                        float vv[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int e = slot * U + u;
-                        vv[u] = __shfl_sync(kFull, v_l, e);
-                        ld_row<VEC>(go[u], frow(JO, __shfl_sync(kFull, c_l[JO], e)), pol_row);
+                        for (int u = 0; u < U; ++u) {
+                            const int e = g0 + slot * U + u;
+                            vv[u] = __shfl_sync(kFull, v_l, e);
+#pragma unroll
+                            for (int jj = 0; jj < NO; ++jj) {
+                                const int j = jj < JF ? jj : jj + 1;
+                                ld_row<VEC>(go[u][jj], frow(j, __shfl_sync(kFull, c_l[j], e)), pol_row);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) {
+                                float p = vv[u];
+#pragma unroll
+                                for (int jj = 0; jj < NO - 1; ++jj) p *= go[u][jj][i];
+                                tacc[i] = fmaf(p, go[u][NO - 1][i], tacc[i]);
+                            }
                     }
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) tacc[i] = fmaf(vv[u], go[u][i], tacc[i]);
                     tpend = true;
                     continue;
                 }

@@ -551,10 +551,14 @@ class _ShardExec:
 def _fiber_flags(plan, rank) -> int:
     """SKRP_FLAG_FIBER_INPUTj for a plan in the fiber layout (tile kernel,
     R = 32, 3 modes): j = position of the fiber mode among the inputs."""
-    if plan.layout != "fibers" or len(plan.shape) != 3 or rank != 32:
+    if plan.layout != "fibers" or (len(plan.shape), rank) not in _FIBER_SHAPES:
         return 0
-    ins = [w for w in range(3) if w != plan.mode]
-    return _lib.FLAG_FIBER_INPUT0 if ins.index(plan.fiber_mode) == 0 else _lib.FLAG_FIBER_INPUT1
+    ins = [w for w in range(len(plan.shape)) if w != plan.mode]
+    return (_lib.FLAG_FIBER_INPUT0, _lib.FLAG_FIBER_INPUT1, _lib.FLAG_FIBER_INPUT2)[ins.index(plan.fiber_mode)]
+
+
+# (modes, rank) with a fiber-reuse kernel instantiation (csrc/mttkrp.cu choose)
+_FIBER_SHAPES = ((3, 32), (4, 64))
 
 
 def choose_fibers(plan, rank, min_fiber=8.0):
@@ -562,10 +566,10 @@ def choose_fibers(plan, rank, min_fiber=8.0):
     fewest rows (the longest (row, c_f) runs), if the expected fiber length
     -- nnz / sum_rows I_f (1 - exp(-n_row / I_f)), the uniform-draw number
     of distinct (row, c_f) pairs -- is at least `min_fiber` (cfg3: ~325 in
-    every mode; cfg2, cfg4: ~1)."""
+    every mode; cfg5 full: ~20 in modes 2 and 3; cfg2, cfg4: ~1)."""
     torch = _torch()
     n, d = len(plan.shape), plan.mode
-    if n != 3 or rank != 32 or plan.nnz == 0:
+    if (n, rank) not in _FIBER_SHAPES or plan.nnz == 0:
         return None
     f = min((w for w in range(n) if w != d), key=lambda w: (plan.shape[w], w))
     rows = plan.coords[d]

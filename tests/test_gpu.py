@@ -1065,3 +1065,26 @@ def test_fiber_reorder_segmented_matches_whole():
         lo, hi = s_.index_range
         assert np.all((rows[s_.start:s_.stop] >= lo) & (rows[s_.start:s_.stop] < hi))
     assert np.array_equal(b._indices, sk.build_mode_plan(t, 0, sk.PartitionConfig(devices=8))._indices)
+
+
+def test_fiber_layout_four_modes():
+    """4-mode fiber layout (R = 64, the cfg5 shape class): every mode picks
+    its smallest input as the fiber mode, the 4-mode fiber instantiation runs
+    (two inputs gathered per nonzero, the fiber row once per run), chained
+    all-mode parity with the oracle under both disciplines."""
+    t = sk.synth_tensor((2000, 3000, 40, 30), 1_000_000, seed=29)
+    fs = sk.random_factors(t.shape, 64, seed=9)
+    for acc in ("atomic", "deterministic-reduce"):
+        plans = sk.build_all_plans(t, sk.PartitionConfig(devices=1))
+        cfg = sk.PlatformConfig(devices=1, rank=64, accumulation=acc, layout="auto")
+        _lib.launch_log(clear=True)
+        outs, _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        assert all(p.layout == "fibers" for p in plans), [p.layout for p in plans]
+        names = [n for _, n in _lib.launch_log()]
+        assert all("mttkrp_v2_kernel<4, 8, 2, 2, " in n and (", 512," in n or ", 1536," in n or ", 2560," in n)
+                   for n in names[:4]), names
+        facs = [f.data.copy() for f in fs]
+        for d in range(4):
+            expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
+            assert rel_err(outs[d], expect) <= TOL
+            facs[d] = outs[d]

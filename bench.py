@@ -153,7 +153,22 @@ def lookup_traffic(config, mode, kernel):
     return None, f"no ncu capture of {want} on {config} mode {mode}"
 
 
-def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world):
+def load_gather_ceiling():
+    """Random 128-B row gathers from a 2-GB table (all DRAM misses), GB/s of
+    row bytes, measured on a B200 by tools/pattern_ceiling.cu (r02r), or None."""
+    path = os.path.join(ROOT, "profiles", "r02", "r02r_pattern_ceiling.jsonl")
+    try:
+        with open(path) as fh:
+            for line in fh:
+                d = json.loads(line)
+                if d.get("part") == "gather_curve":
+                    return max((p["row_gbs"] for p in d["points"] if p["table_mb"] == 2048), default=None)
+    except Exception:
+        return None
+    return None
+
+
+def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world, seq=None):
     """Roofline of the dominant (MTTKRP) kernel per mode.  `frac` uses the
     bytes the kernel really moves: DRAM read + write per launch from the ncu
     --set full capture of EXACTLY the launched template instantiation
@@ -161,7 +176,11 @@ def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src
     over the live per-launch time measured here with CUDA events.  The
     SURVEY.md §8(d) algorithmic figure (every gather charged to HBM; > 1 when
     L2 serves gathers) is `frac_algorithmic`; the compulsory lower bound
-    (stream once, each factor once, output once) is `frac_compulsory`."""
+    (stream once, each factor once, output once) is `frac_compulsory`.
+    `frac_miss_pattern` (needs `seq` = the sequential metadata bytes per
+    mode): the DRAM floor of the kernel's own traffic -- metadata at the copy
+    peak, every other DRAM byte at the measured random 128-B gather rate --
+    over the live kernel time."""
     import torch
 
     from paper_2507_15121_b200 import _lib
@@ -171,7 +190,8 @@ def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src
     torch.cuda.synchronize()
     log = _lib.launch_log()
     names = [sorted({n for m, n in log if m == d}) for d in modes]
-    per_mode, traffic, missing = [], [], []
+    per_mode, traffic, missing, floors = [], [], [], []
+    gceil = load_gather_ceiling()
     for i, d in enumerate(modes):
         ent, why = (None, "N > 1: ncu captures are single-GPU") if world > 1 else (
             lookup_traffic(config, d, names[i][0]) if len(names[i]) == 1 else (None, "several kernels per mode"))
@@ -185,6 +205,10 @@ def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src
                          "frac_dram": t / kern[i] / 1e9 / peak if t else None,
                          "frac_algorithmic": alg[i] / kern[i] / 1e9 / peak,
                          "frac_compulsory": comp[i] / kern[i] / 1e9 / peak})
+        if t and gceil and seq is not None:
+            fl = seq[i] / peak / 1e9 + max(0.0, t - seq[i]) / gceil / 1e9
+            floors.append(fl)
+            per_mode[-1].update({"miss_pattern_floor_ms": fl * 1e3, "frac_miss_pattern": fl / kern[i]})
     ach_alg = sum(alg) / sum(kern) / 1e9
     if all(t is not None for t in traffic):
         achieved, basis = sum(traffic) / sum(kern) / 1e9, "measured DRAM bytes (ncu, same kernel) / live kernel time"
@@ -197,7 +221,11 @@ def roofline_block(config, modes, runner, dev_f, kern, alg, comp, peak, peak_src
             "kernel_ms_per_mode": [k * 1e3 for k in kern], "algorithmic_bytes_per_mode": alg,
             "compulsory_bytes_per_mode": comp, "achieved_algorithmic": ach_alg,
             "frac_algorithmic": ach_alg / peak, "frac_compulsory": sum(comp) / sum(kern) / 1e9 / peak,
-            "per_mode": per_mode}
+            "per_mode": per_mode,
+            "frac_miss_pattern": sum(floors) / sum(kern) if floors and len(floors) == len(modes) else None,
+            "random_gather_gbs": gceil,
+            "miss_pattern_basis": "metadata bytes at the copy peak + all other ncu DRAM bytes at the measured "
+                                  "random 128-B gather rate (profiles/r02/r02r_pattern_ceiling.jsonl), / live time"}
 
 
 def algorithmic_bytes(shape, nnz, rank, mode):
@@ -687,7 +715,8 @@ def run_ours(args, cfg):
             + sum(shape[w] * R * 4 for w in range(len(shape)) if w != plans[i].mode)
             + runner.owned_rows(i) * R * 4 for i in range(len(modes))]
     balance = plan_balance(plans)
-    roof = roofline_block(args.config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world)
+    seq = [runner.local_nnz(i) * (4 * len(shape) + 4) for i in range(len(modes))]
+    roof = roofline_block(args.config, modes, runner, dev_f, kern, alg, comp, peak, peak_src, world, seq)
 
     # ---- end to end through the public runner with pinned host buffers:
     # every step uploads the factors it reads and downloads all outputs;
@@ -918,7 +947,8 @@ def run_cpd(args, cfg, plans, runner, dev_f, dev, world, rank, local_gpu, setup_
     shape, R = cfg["shape"], cfg["rank"]
     comp = [runner.local_nnz(i) * (4 * nm + 4) + sum(shape[w] * R * 4 for w in range(nm) if w != plans[i].mode)
             + runner.owned_rows(i) * R * 4 for i in range(nm)]
-    roof = roofline_block(args.config, list(range(nm)), runner, dev_f, kern, alg, comp, peak, peak_src, world)
+    seq = [runner.local_nnz(i) * (4 * nm + 4) for i in range(nm)]
+    roof = roofline_block(args.config, list(range(nm)), runner, dev_f, kern, alg, comp, peak, peak_src, world, seq)
     roof["mttkrp_share_of_iteration"] = sum(kern) / step_s
     parity = None
     if tensor is not None or samples is not None:

@@ -460,3 +460,18 @@ def test_bench_roofline_matches_exact_kernel():
     assert ent is None and "no ncu capture" in why
     ent, _ = bench.lookup_traffic("cfg2", 2, "void skrp::mttkrp_v2_kernel<3, 4, 4, 2, 66, 1>(skrp_mttkrp_args, int)")
     assert ent is None
+
+
+def test_bench_miss_pattern_floor():
+    """The miss-pattern floor bench.py reports: metadata at the copy peak plus
+    every other ncu DRAM byte at the measured random-gather rate -- for the
+    cfg2 mode-0 tile kernel capture it lands at ~42 ms."""
+    import bench
+
+    g = bench.load_gather_ceiling()
+    assert g is not None and 3000 < g < 8000
+    ent, _ = bench.lookup_traffic("cfg2", 0, "void skrp::mttkrp_v2_kernel<3, 4, 4, 2, 66, 1>(skrp_mttkrp_args, int)")
+    seq = 1_700_000_000 * 16
+    peak, _ = bench.load_peaks()
+    floor_ms = (seq / peak + (ent["traffic_bytes_per_launch"] - seq) / g) / 1e9 * 1e3
+    assert 35.0 < floor_ms < 50.0

@@ -2,6 +2,7 @@
 # round-2 final evidence (latest code: fibers auto for cfg3/cfg5): GPU suite, bench lines, launch list
 o=gpurun_out/r02t; mkdir -p $o
 timeout 2400 python -m pytest tests/ -q -m gpu > $o/pytest_gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.txt 2>&1
 timeout 900 python bench.py --steps 20 --warmup 5 > $o/bench_cfg2.json 2> $o/bench_cfg2.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $o/bench_reference.json 2> $o/bench_reference.err
 timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --accumulation deterministic-reduce > $o/bench_cfg2_det.json 2> $o/bench_cfg2_det.err

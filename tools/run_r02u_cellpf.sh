@@ -1,4 +1,6 @@
 #!/bin/bash
+# r02u (historical): variants 2-4 (block bulk prefetch) were removed after this sweep
+# (profiles/sweeps/r02s_cells_wide_negative.jsonl); only variants 0 and 1 remain.
 # cells kernel: bulk L2 prefetch of the blocks cell c+PFD brings in (variants 2-4)
 o=gpurun_out/r02u; mkdir -p $o
 timeout 900 python -m pytest tests/test_gpu_cells.py -x -q > $o/cells_tests.txt 2>&1

@@ -475,3 +475,35 @@ def test_bench_miss_pattern_floor():
     peak, _ = bench.load_peaks()
     floor_ms = (seq / peak + (ent["traffic_bytes_per_launch"] - seq) / g) / 1e9 * 1e3
     assert 35.0 < floor_ms < 50.0
+
+
+def test_metrics_records_match_reference_golden():
+    """run_records / write_records reproduce the reference's records exactly
+    (tests/golden/metrics_records.json, written by make_metrics_golden.py from
+    the reference's own metrics module)."""
+    import io
+    import json
+    import os
+
+    from paper_2507_15121_b200 import metrics as M
+
+    # the same run as tests/golden/make_metrics_golden.py
+    def sample(mod):
+        ms = [mod.ModeMetrics(d, [0.1 * d + 0.01, 0.2, 0.05 * (d + 1)], [10 + d, 20, 30], [1, 2, 3],
+                              staging_bytes=5 * d, staging_seconds=0.1, allgather_bytes=7, allgather_seconds=0.2 * d,
+                              barrier_count=d, wall_seconds=0.3) for d in range(3)]
+        return mod.RunMetrics(3, ms, [0.5, 0.25, 0.125], 1.5)
+
+    class Platform:
+        devices, workers_per_device, column_width, rank, accumulation, scheduling = 3, 1, 32, 16, "atomic", "dynamic"
+
+    class Tensor:
+        name, shape, nnz = "golden", (3, 4, 5), 60
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "metrics_records.json")) as fh:
+        want = json.load(fh)
+    got = M.run_records(sample(M), Platform, Tensor)
+    assert got == want
+    buf = io.StringIO()
+    M.write_records(got, buf)
+    assert [json.loads(line) for line in buf.getvalue().splitlines()] == want

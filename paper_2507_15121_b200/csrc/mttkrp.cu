@@ -425,9 +425,9 @@ static Variant choose(const skrp_mttkrp_args &a)
             !(a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1))) {
             // 4-mode fiber layout (cfg5): two gathered inputs per nonzero, the
             // fiber input's row once per run
-            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<4, 8, 2, 2, 512, 1>();
-            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<4, 8, 2, 2, 512 | 1024, 1>();
-            return mk2<4, 8, 2, 2, 512 | 2048, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<4, 8, 2, 2, 512 | 4096, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<4, 8, 2, 2, 512 | 1024 | 4096, 1>();
+            return mk2<4, 8, 2, 2, 512 | 2048 | 4096, 1>();
         }
         if (a.nmodes == 3 && a.rank == 32) {
             return mk2<3, 4, 4, 2, 64, 1>();

@@ -75,14 +75,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     // fiber ends (acc += t * F[f]) -- half the gathered bytes on long fibers
     constexpr bool FIB = (PLAIN & 512) != 0;
     constexpr int JF = (PLAIN >> 10) & 3;  // bits 1024 / 2048: the fiber input
-    // PLAIN bit 4096 (with FIB): twice the row loads in flight on fiber runs
-    // -- G < 32: two groups of the batch at a time; G == 32: the metadata
-    // pipeline runs two batches ahead and a fiber-uniform batch whose
-    // successor continues the same (row, fiber) takes both at once
+    // PLAIN bit 4096 (with FIB, G < 32): a fiber-uniform batch issues two
+    // groups' row loads before folding either -- twice the loads in flight on
+    // fiber runs (the G == 32 analogue, two batches per step with the metadata
+    // two batches ahead, spills at 128 registers: DESIGN.md §4)
     constexpr bool FIB2 = FIB && (PLAIN & 4096) != 0;
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     static_assert(!FIB || (STREAMED == 0 && JF < NIN), "fiber reuse: no streamed input");
-    static_assert(!FIB2 || G == 32 || 32 % (2 * G) == 0, "paired fiber groups must tile the batch");
+    static_assert(!FIB2 || (G < 32 && 32 % (2 * G) == 0), "paired fiber groups must tile the batch");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -266,23 +266,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         auto advance = [&](int64_t base) {
             if (base + 32 < b1) fetch(base + 32);
         };
-        uint32_t mr_l = 0, mc_l[NIN];
-        float mv_l = 0.f;
-#pragma unroll
-        for (int j = 0; j < NIN; ++j) mc_l[j] = 0;
-        constexpr bool DEEP = FIB2 && G == 32;
-        // DEEP: batch base+32 in n*_l (arrived), base+64 in flight in m*_l
-        auto shift2 = [&](int64_t base_) {
-            nr_l = mr_l;
-            nv_l = mv_l;
-#pragma unroll
-            for (int j = 0; j < NIN; ++j) nc_l[j] = mc_l[j];
-            if (base_ + 64 < b1) fetch_to(base_ + 64, mr_l, mv_l, mc_l);
-        };
         fetch(b0);
-        if constexpr (DEEP) {
-            if (b0 + 32 < b1) fetch_to(b0 + 32, mr_l, mv_l, mc_l);
-        }
         for (int64_t base = b0; base < b1; base += 32) {
             // a short last batch is padded with copies of its last nonzero
             // carrying value 0: same row (no extra boundary), valid
@@ -293,8 +277,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
             uint32_t c_l[NIN];
 #pragma unroll
             for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
-            if constexpr (DEEP) shift2(base);
-            else advance(base);
+            advance(base);
             const bool uniform = __all_sync(kFull, r_l == cur);
             if constexpr (FIB) {
                 if (__all_sync(kFull, r_l == cur && c_l[JF] == curf)) {
@@ -332,18 +315,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                             gather(gb, vb, g0 + G, v_l, c_l);
                             fold(ga, va);
                             fold(gb, vb);
-                        }
-                    } else if constexpr (DEEP) {
-                        // the next batch (arrived) continues the same fiber: take both
-                        const bool two = base + 64 <= b1 && __all_sync(kFull, nr_l == cur && nc_l[JF] == curf);
-                        float ga[U][NO][VEC], gb[U][NO][VEC], va[U], vb[U];
-                        gather(ga, va, 0, v_l, c_l);
-                        if (two) gather(gb, vb, 0, nv_l, nc_l);
-                        fold(ga, va);
-                        if (two) {
-                            fold(gb, vb);
-                            base += 32;
-                            shift2(base);
                         }
                     } else {
 #pragma unroll 1

@@ -78,6 +78,29 @@ __device__ __forceinline__ uint64_t policy_evict_last()
     return p;
 }
 
+// 4-byte cp.async into shared memory (src_size 0: zero-fill), L2 policy hint
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, int src_size, uint64_t pol)
+{
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;" ::"r"(dst), "l"(src),
+                 "r"(src_size), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p, uint64_t pol)
 {
     uint32_t v;

@@ -351,7 +351,7 @@ static Variant mk2()
 {
     Variant v;
     v.v2 = mttkrp_v2_kernel<NM, LPN, U, MINB, PLAIN, TRED>;
-    v.smem = v2_smem_bytes<8 * LPN>();
+    v.smem = v2_smem_bytes<8 * LPN, (PLAIN & 8192) ? NM + 1 : 0>();
     return v;
 }
 
@@ -418,8 +418,8 @@ static Variant choose(const skrp_mttkrp_args &a)
             if (sm == SKRP_FLAG_STREAM_INPUT0) return mk2<3, 4, 4, 2, 64 | 2, 1>();
             if (sm == SKRP_FLAG_STREAM_INPUT1) return mk2<3, 4, 4, 2, 64 | 4, 1>();
             // fiber layout: the fiber input's row is gathered once per (row, fiber) run
-            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<3, 4, 4, 2, 64 | 512, 1>();
-            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<3, 4, 4, 2, 64 | 512 | 1024, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT0) return mk2<3, 4, 4, 2, 64 | 512 | 8192, 1>();
+            if (a.flags & SKRP_FLAG_FIBER_INPUT1) return mk2<3, 4, 4, 2, 64 | 512 | 1024 | 8192, 1>();
         }
         if (a.nmodes == 4 && a.rank == 64 && (a.flags & SKRP_FLAG_FIBER_MASK) &&
             !(a.flags & (SKRP_FLAG_STREAM_INPUT0 | SKRP_FLAG_STREAM_INPUT1))) {

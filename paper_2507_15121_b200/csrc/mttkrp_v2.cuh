@@ -80,14 +80,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     // fiber runs (the G == 32 analogue, two batches per step with the metadata
     // two batches ahead, spills at 128 registers: DESIGN.md §4)
     constexpr bool FIB2 = FIB && (PLAIN & 4096) != 0;
+    // PLAIN bit 8192 (with FIB, G == 32): the batch metadata runs two batches
+    // ahead through a 3-slot cp.async ring in shared memory (no registers
+    // held), and a fiber-uniform batch whose successor continues the same
+    // (row, fiber) gathers both batches' rows before folding either
+    constexpr bool SMETA = FIB && (PLAIN & 8192) != 0;
+    constexpr int NA = NIN + 2;  // ring arrays: row, inputs, value
     static_assert(32 % G == 0, "groups must tile the 32-nonzero batch");
     static_assert(!FIB || (STREAMED == 0 && JF < NIN), "fiber reuse: no streamed input");
     static_assert(!FIB2 || (G < 32 && 32 % (2 * G) == 0), "paired fiber groups must tile the batch");
+    static_assert(!SMETA || G == 32, "two-batch fiber steps: one group per batch");
     extern __shared__ __align__(16) float smem_v2[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     float *stage = smem_v2 + (size_t)wib * (33 * STR);  // 32 nonzero rows + 1 carry row
     float *carry_row = stage + 32 * STR;
+    // SMETA ring: 3 slots x NA arrays x 32 words per warp, after the stages
+    const uint32_t mring_s = (uint32_t)__cvta_generic_to_shared(smem_v2 + (size_t)kWarpsPerCta * (33 * STR)) +
+                             (uint32_t)(wib * 3 * NA * 32 * 4);
     const int slot = lane / LPN, sl = lane % LPN;
     const int col = sl * VEC;
     const int mode = a.mode;
@@ -266,18 +276,54 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
         auto advance = [&](int64_t base) {
             if (base + 32 < b1) fetch(base + 32);
         };
-        fetch(b0);
-        for (int64_t base = b0; base < b1; base += 32) {
+        // SMETA: batch at nbase -> ring slot k (lane-private words; a short
+        // batch is padded like fetch_to: last nonzero, value 0 by zero-fill)
+        auto sfetch = [&](int64_t nbase, int k) {
+            if (nbase < b1) {
+                const int nn = (b1 - nbase) < 32 ? (int)(b1 - nbase) : 32;
+                const bool v = lane < nn;
+                const int64_t src = nbase + (v ? lane : nn - 1);
+                const uint32_t sb = mring_s + (uint32_t)((k * NA * 32 + lane) * 4);
+                cp_async4(sb, rowc + src, 4, pol_stream);
+#pragma unroll
+                for (int j = 0; j < NIN; ++j) cp_async4(sb + (1 + j) * 128, C[j] + src, 4, pol_stream);
+                cp_async4(sb + (NA - 1) * 128, a.values + src, v ? 4 : 0, pol_stream);
+            }
+            cp_async_commit();
+        };
+        auto sread = [&](int k, uint32_t &r, float &vv, uint32_t (&c)[NIN]) {
+            const uint32_t sb = mring_s + (uint32_t)((k * NA * 32 + lane) * 4);
+            r = lds_u32(sb);
+#pragma unroll
+            for (int j = 0; j < NIN; ++j) c[j] = lds_u32(sb + (1 + j) * 128);
+            vv = __uint_as_float(lds_u32(sb + (NA - 1) * 128));
+        };
+        int kslot = 0;  // SMETA: ring slot of the batch at `base`
+        if constexpr (SMETA) {
+            sfetch(b0, 0);
+            sfetch(b0 + 32, 1);
+        } else {
+            fetch(b0);
+        }
+        for (int64_t base = b0; base < b1; base += 32, kslot = kslot == 2 ? 0 : kslot + 1) {
             // a short last batch is padded with copies of its last nonzero
             // carrying value 0: same row (no extra boundary), valid
             // addresses, zero contribution -- so no per-element predicates
             const int nin = (b1 - base) < 32 ? (int)(b1 - base) : 32;
-            const uint32_t r_l = nr_l;
-            const float v_l = nv_l;
+            uint32_t r_l;
+            float v_l;
             uint32_t c_l[NIN];
+            if constexpr (SMETA) {
+                cp_async_wait<1>();  // this batch landed (the next may be in flight)
+                sread(kslot, r_l, v_l, c_l);
+                sfetch(base + 64, kslot == 0 ? 2 : kslot - 1);
+            } else {
+                r_l = nr_l;
+                v_l = nv_l;
 #pragma unroll
-            for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
-            advance(base);
+                for (int j = 0; j < NIN; ++j) c_l[j] = nc_l[j];
+                advance(base);
+            }
             const bool uniform = __all_sync(kFull, r_l == cur);
             if constexpr (FIB) {
                 if (__all_sync(kFull, r_l == cur && c_l[JF] == curf)) {
@@ -315,6 +361,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
                             gather(gb, vb, g0 + G, v_l, c_l);
                             fold(ga, va);
                             fold(gb, vb);
+                        }
+                    } else if constexpr (SMETA) {
+                        // the next batch (landed: all but the newest group
+                        // complete) continues the same fiber: take both
+                        cp_async_wait<1>();
+                        const int k1 = kslot == 2 ? 0 : kslot + 1;
+                        const uint32_t sb1 = mring_s + (uint32_t)((k1 * NA * 32 + lane) * 4);
+                        const bool two = base + 64 <= b1 &&
+                                         __all_sync(kFull, lds_u32(sb1) == cur && lds_u32(sb1 + (1 + JF) * 128) == curf);
+                        float ga[U][NO][VEC], va[U];
+                        gather(ga, va, 0, v_l, c_l);
+                        if (two) {
+                            uint32_t r2, c2[NIN];
+                            float v2;
+                            sread(k1, r2, v2, c2);
+                            float gb[U][NO][VEC], vb[U];
+                            gather(gb, vb, 0, v2, c2);
+                            fold(ga, va);
+                            fold(gb, vb);
+                            base += 32;
+                            kslot = k1;
+                            sfetch(base + 64, kslot == 0 ? 2 : kslot - 1);
+                        } else {
+                            fold(ga, va);
                         }
                     } else {
 #pragma unroll 1
@@ -534,8 +604,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB)
     }
 }
 
-template <int RR>
+template <int RR, int META_ARRAYS = 0>
 constexpr size_t v2_smem_bytes()
 {
-    return sizeof(float) * kWarpsPerCta * (33 * (RR + 4));
+    return sizeof(float) * kWarpsPerCta * (33 * (RR + 4) + 3 * 32 * META_ARRAYS);
 }

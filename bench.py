@@ -558,7 +558,8 @@ def run_ours(args, cfg):
                            layout="panel" if args.fused_allgather else args.layout, l2_budget_mb=args.l2_mb,
                            max_blocks=args.max_blocks, fused_allgather=args.fused_allgather,
                            cell_lag=args.cell_lag, cell_variant=args.cell_variant, cell_outer_mb=args.cell_outer_mb,
-                           cell_inner_mb=args.cell_inner_mb, cell_keep_arrays=False)
+                           cell_inner_mb=args.cell_inner_mb, cell_keep_arrays=False,
+                           panel_smem_kb=args.panel_smem_kb)
 
     from paper_2507_15121_b200.engine import apply_layout
 
@@ -1100,6 +1101,8 @@ def main():
     ap.add_argument("--cell-variant", type=int, default=1, help="cells layout: kernel variant (csrc/mttkrp_cells.cu)")
     ap.add_argument("--cell-outer-mb", type=int, default=32)
     ap.add_argument("--cell-inner-mb", type=int, default=8)
+    ap.add_argument("--panel-smem-kb", type=int, default=64,
+                    help="panel layout (deterministic-reduce): shared memory for the output slab")
     ap.add_argument("--l2-mb", type=int, default=192)
     ap.add_argument("--max-blocks", type=int, default=8)
     ap.add_argument("--shifts", default="", help="force block shifts per mode, e.g. '-1,19,18;19,-1,18;19,18,-1'")

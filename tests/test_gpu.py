@@ -1093,3 +1093,32 @@ def test_fiber_layout_four_modes():
             expect = oracle.mttkrp_seq_c(t.indices, t.values, facs, d)
             assert rel_err(outs[d], expect) <= TOL
             facs[d] = outs[d]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rank,tile", [(32, 33), (32, 100), (32, 1000), (64, 37), (64, 1000)])
+def test_fiber_odd_tiles(rank, tile):
+    """Fiber instantiations with tiles that are not a multiple of the 32-
+    nonzero batch: short last batches inside fiber runs, the R = 32 two-batch
+    step's end test (base + 64 <= tile end) and the metadata ring's empty
+    tail groups, the R = 64 paired groups -- every mode within tolerance of
+    the oracle, atomic and deterministic-reduce agreeing to tolerance."""
+    nm = 3 if rank == 32 else 4
+    shape = (40, 500, 60) if nm == 3 else (30, 400, 300, 20)
+    t = sk.synth_tensor(shape, 400_000, seed=23)
+    fs = sk.random_factors(t.shape, rank, seed=6)
+    facs = [f.data.copy() for f in fs]
+    outs = {}
+    for acc in ("atomic", "deterministic-reduce"):
+        plans = sk.build_all_plans(t, sk.PartitionConfig(devices=1))
+        cfg = sk.PlatformConfig(devices=1, rank=rank, accumulation=acc, layout="fibers", tile_nnz=tile)
+        _lib.launch_log(clear=True)
+        outs[acc], _ = sk.mttkrp_all_modes(plans, sk.make_devices(fs, cfg), cfg)
+        names = [n for _, n in _lib.launch_log() if "mttkrp_v2_kernel<" in n]
+        assert names and all(_plain_bits(n) & 512 for n in names), names
+    f2 = [f.copy() for f in facs]
+    for d in range(nm):
+        expect = oracle.mttkrp_seq_c(t.indices, t.values, f2, d)
+        for acc in outs:
+            assert rel_err(outs[acc][d], expect) <= TOL, (acc, d)
+        f2[d] = outs["atomic"][d]
